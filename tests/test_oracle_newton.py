@@ -1,0 +1,180 @@
+"""Pins of the oracle's Newton machinery against independent mathematics.
+
+* Jacobian = directional finite differences of the residual (first-order agreement).
+* Banded LU / BiCGSTAB = numpy (pivoted LAPACK) dense solves of the assembled operator.
+* Sequential BDF1 + Newton = brute-force dense Newton on the WHOLE space-time system of Eq. (4)
+  with a finite-difference Jacobian and numpy.linalg.solve (tiny grids): pins Theorem 1's claim that
+  the all-at-once and sequential solutions coincide.
+* All-at-once mode = sequential solution; quadratic Newton decay.
+* Theorem 1 product form = block forward substitution = dense block solve.
+* Invariants: periodic mass conservation, constant states, x<->y symmetry, heat energy decay.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from oracle import product_form as PF
+from paper_2406_00878_b200 import workloads as W
+
+
+def _cases():
+    rng = np.random.default_rng(11)
+    out = []
+    # Dirichlet heat with a nonzero time-dependent ring, non-square grid
+    p = W.paper_heat(7, nt=3)
+    p.m2 = 5e-4
+    out.append(p)
+    # Dirichlet Burgers with a ring
+    q = W.paper_burgers(8, mu=0.02, nt=3)
+    out.append(q)
+    # periodic Burgers and periodic nonlinear heat, random data, nx != ny
+    out.append(W.custom("pb", W.BURGERS, W.PERIODIC, 6, 5, 3, 0.05, 0.02, 0.0, u0=rng.standard_normal(30)))
+    out.append(W.custom("ph", W.HEAT, W.PERIODIC, 5, 7, 3, 0.01, 0.5, 0.7, u0=rng.standard_normal(35)))
+    # Dirichlet heat with mu = m0 + m2 u^2 and unequal spacings
+    out.append(W.custom("dh", W.HEAT, W.DIRICHLET, 6, 5, 3, 0.01, 1.0, 1.0, u0=rng.standard_normal(20),
+                        ring=rng.standard_normal((3, 22)), domain=(0.0, 1.0, 0.0, 0.6)))
+    return out
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_jacobian_matches_finite_differences(case):
+    p = _cases()[case]
+    rng = np.random.default_rng(case)
+    u = p.u0 + 0.3 * rng.standard_normal(p.ns)
+    uprev = p.u0.copy()
+    A = O.to_dense(p, O.jacobian(p, u, n=2))
+    w = rng.standard_normal(p.ns)
+    G0 = O.residual(p, u, uprev, n=2)
+    errs = []
+    for eps in (1e-3, 1e-4, 1e-5):
+        fd = (O.residual(p, u + eps * w, uprev, n=2) - O.residual(p, u - eps * w, uprev, n=2)) / (2 * eps)
+        errs.append(np.abs(fd - A @ w).max() / np.abs(A @ w).max())
+    assert errs[-1] < 1e-8
+    # dG^n/du^{n-1} = -I (the sub-diagonal of Eq. (6))
+    fd_prev = (O.residual(p, u, uprev + 1e-6 * w, n=2) - G0) / 1e-6
+    assert np.abs(fd_prev + w).max() < 1e-8
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_linear_solvers_match_dense_lapack(case):
+    p = _cases()[case]
+    rng = np.random.default_rng(100 + case)
+    u = p.u0 + 0.3 * rng.standard_normal(p.ns)
+    coefs = O.jacobian(p, u, n=1)
+    A = O.to_dense(p, coefs)
+    b = rng.standard_normal(p.ns)
+    x_ref = np.linalg.solve(A, b)
+    if p.bc == W.DIRICHLET:
+        x = O.band_lu_solve(p, coefs, b)
+        assert np.abs(x - x_ref).max() <= 1e-12 * np.abs(x_ref).max()
+    x2 = O.bicgstab_solve(p, coefs, b)
+    assert np.abs(x2 - x_ref).max() <= 1e-12 * np.abs(x_ref).max()
+
+
+def test_band_lu_vs_bicgstab_larger_dirichlet():
+    p = W.config(1, n=40, nt=1)
+    coefs = O.jacobian(p, p.u0, n=1)
+    b = np.random.default_rng(3).standard_normal(p.ns)
+    x1 = O.band_lu_solve(p, coefs, b)
+    x2 = O.bicgstab_solve(p, coefs, b)
+    assert np.abs(x1 - x2).max() <= 1e-13 * np.abs(x1).max()
+    assert np.abs(O.matvec(p, coefs, x1) - b).max() < 1e-13 * np.abs(b).max()
+
+
+def _global_residual(p, Uflat):
+    U = Uflat.reshape(p.nt, p.ns)
+    return np.concatenate([O.residual(p, U[n], p.u0 if n == 0 else U[n - 1], n=n + 1) for n in range(p.nt)])
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_sequential_equals_bruteforce_global_newton(case):
+    """Brute force: Newton on the whole space-time system of Eq. (4) (<= 4x4x3-sized), Jacobian by
+    central finite differences, dense pivoted solve; must land on the sequential oracle's solution."""
+    p = _cases()[case]
+    N = p.nt * p.ns
+    U = np.tile(p.u0, p.nt)
+    for it in range(40):
+        F = _global_residual(p, U)
+        J = np.empty((N, N))
+        for k in range(N):
+            e = np.zeros(N)
+            e[k] = 1e-6
+            J[:, k] = (_global_residual(p, U + e) - _global_residual(p, U - e)) / 2e-6
+        d = np.linalg.solve(J, -F)
+        U = U + d
+        if np.abs(d).max() < 1e-14 * max(1, np.abs(U).max()):
+            break
+    assert np.abs(_global_residual(p, U)).max() < 1e-14 * max(1.0, np.abs(U).max()) * 100
+    seq = O.solve_sequential(p)
+    assert seq.status == 0
+    assert np.abs(seq.U.reshape(-1) - U).max() <= 1e-12 * max(1.0, np.abs(U).max())
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_allatonce_equals_sequential_and_is_quadratic(cfg):
+    p = W.config(cfg) if cfg == 1 else W.config(2, n=24, nt=12)
+    seq = O.solve_sequential(p)
+    aao = O.solve_allatonce(p, tol=1e-12)
+    assert aao.status in (0, 1)
+    scale = np.abs(seq.U).max()
+    assert np.abs(aao.U - seq.U).max() <= 1e-13 * scale
+    d = aao.hist[:, 3]
+    # quadratic decay over the pre-floor tail: |d_{k+1}| <= C |d_k|^2
+    tail = [k for k in range(len(d) - 1) if d[k + 1] > 1e-13]
+    for k in tail[1:]:
+        assert d[k + 1] <= 50.0 * d[k] ** 2, (k, d)
+    assert d[-1] <= 1e-12
+
+
+def test_theorem1_product_form_random_instances():
+    """Theorem 1: the decoupled P^n dv^n = r~^n equals Eq. (6)'s solution."""
+    rng = np.random.default_rng(7)
+    for trial in range(100):
+        L = int(rng.integers(1, 4))
+        m = int(rng.integers(2, 7))
+        A = [np.eye(m) * 3 + rng.standard_normal((m, m)) for _ in range(L)]
+        r = [rng.standard_normal(m) for _ in range(L)]
+        ref = PF.dense_block_solve(A, r)
+        for got in (PF.product_form_solve(A, r), PF.product_form_solve(A, r, diag_scaling=True),
+                    PF.forward_recursion(A, r)):
+            for g, e in zip(got, ref):
+                assert np.abs(g - e).max() <= 1e-12 * max(1, np.abs(e).max())
+
+
+def test_remark1_order_matters():
+    """Remark 1: A_i A_j != A_j A_i, and the wrong product order gives a wrong dv."""
+    rng = np.random.default_rng(8)
+    A = [PF.five_point_pattern(4, 4, rng) for _ in range(3)]
+    r = [rng.standard_normal(16) for _ in range(3)]
+    assert np.abs(A[0] @ A[1] - A[1] @ A[0]).max() > 1e-3
+    good = PF.product_form_solve(A, r)
+    bad = PF.product_form_solve(A[::-1], r)
+    assert np.abs(good[2] - bad[2]).max() > 1e-6
+
+
+def test_periodic_burgers_conserves_mass():
+    p = W.config(2, n=16, nt=6)
+    r = O.solve_sequential(p)
+    m0 = p.u0.sum()
+    for n in range(p.nt):
+        assert abs(r.U[n].sum() - m0) < 1e-12
+
+
+def test_constant_state_is_fixed_point():
+    p = W.custom("const", W.BURGERS, W.PERIODIC, 8, 8, 4, 0.01, 0.01, 0.0, u0=np.full(64, 0.37))
+    r = O.solve_sequential(p)
+    assert np.abs(r.U - 0.37).max() < 1e-15
+    q = W.custom("consth", W.HEAT, W.DIRICHLET, 8, 8, 4, 0.01, 1.0, 1.0, u0=np.full(49, 2.0),
+                 ring=np.full((4, 32), 2.0))
+    r = O.solve_sequential(q)
+    assert np.abs(r.U - 2.0).max() < 1e-14
+
+
+def test_xy_symmetry_and_heat_energy_decay():
+    p = W.config(1)
+    r = O.solve_sequential(p)
+    for n in range(p.nt):
+        F = r.U[n].reshape(p.nyu, p.nxu)
+        assert np.abs(F - F.T).max() < 1e-14
+    e = [np.linalg.norm(p.u0)] + [np.linalg.norm(r.U[n]) for n in range(p.nt)]
+    assert all(e[k + 1] < e[k] for k in range(len(e) - 1))
