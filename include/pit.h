@@ -1,0 +1,156 @@
+/*
+ * pit.h — C ABI of libpit: the all-at-once (parallel-in-time) Newton iteration for the implicit
+ * BDF1 discretization of 2-D nonlinear heat / viscous Burgers equations ("ParaDIn",
+ * arXiv 2406.00878), hand-written CUDA for sm_100a (B200), fp64 throughout.
+ *
+ * Citations: "PAPER.md:L" = line L of the paper's LaTeX source (/root/reference/PAPER.md at build
+ * time; the text is not needed at run time).
+ *
+ * What a solve computes (Eqs. (4)-(6)): the space-time solution U = [u^1 .. u^Nt]
+ * of
+ *     (u^n - u^{n-1})/tau + F(u^n) = q^n,   n = 1..Nt                             (Eq. 4)
+ * where F is the 5-point discretization of Eq. (3) of
+ *     u_t + f(u)_x + g(u)_y = (mu(u) u_x)_x + (mu(u) u_y)_y                       (Eq. 1)
+ * with f = g = u^2/2 (Burgers) or 0 (heat), mu(u) = m0 + m2 u^2, face viscosity
+ * mu_{i+1/2} = mu((u_i + u_{i+1})/2), and Dirichlet (Eq. 2) or periodic boundaries.  It is solved by
+ * Newton's method for ALL levels at once (Eq. 5): every iteration forms the space-time residual and
+ * the block-bidiagonal Jacobian of Eq. (6) (kernel a), applies its exact blockwise inverse Eq. (7)
+ * (stage b: on-device level recurrence, or the literal Theorem 1 product form inside the paper's
+ * Section 7 conditioning window), solves the per-level 5-point systems (stage c, batched
+ * BiCGSTAB) and updates U, with convergence checked on the device (stage d).
+ *
+ * Conventions
+ *   Layout: fp64, row-major [n][j][i], i (x) fastest.  Level n = 1..nt is stored
+ *           at index n-1; u^0 is an input, not an unknown.
+ *   Grid:   nx, ny count grid INTERVALS.  Unknowns per level:
+ *           Dirichlet (nx-1)*(ny-1) at the interior nodes; periodic nx*ny.
+ *   Dirichlet ring (per level, at t^n = n*dt): bottom j=0 (i=0..nx), top j=ny (i=0..nx),
+ *           left i=0 (j=1..ny-1), right i=nx (j=1..ny-1): 2*(nx+ny) values.
+ *   Ownership: the caller owns every buffer passed in; the library never keeps a caller pointer past
+ *           the return of pit_solve, or past completion of the stream work of pit_*_device.
+ *           The handle owns all internal device memory (pit_destroy frees it).
+ *   Threading: a handle is not thread-safe (one solve at a time); distinct handles are independent.
+ *   Errors: every entry point returns a pit_status; negative = error.  pit_last_error(h) gives
+ *           detail.  No CPU fallback exists: without a usable sm_100 device pit_create fails with
+ *           PIT_ECUDA.
+ *   Determinism: identical inputs and configuration on the same GPU give bit-identical outputs
+ *           (fixed-order reductions, no floating-point atomics).
+ */
+#ifndef PIT_H
+#define PIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PIT_ABI_VERSION 1
+
+typedef enum {
+    PIT_OK = 0,           /* converged: max|dU_k| <= newton_tol */
+    PIT_OK_FLOOR = 1,     /* converged at the rounding floor (stop rule (2) below) */
+    PIT_EINVAL = -1,      /* invalid argument / configuration / ABI mismatch */
+    PIT_ENOMEM = -2,      /* device allocation failed */
+    PIT_ECUDA = -3,       /* CUDA error or no usable sm_100 device (detail: pit_last_error) */
+    PIT_ENOCONV = -4,     /* newton_max reached; outputs hold the last iterate and the histories */
+    PIT_EBREAKDOWN = -5,  /* Krylov breakdown or NaN/Inf detected on the device */
+    PIT_ECOND = -6        /* product-form window forced beyond the Section 7 conditioning gate */
+} pit_status;
+
+enum { PIT_HEAT = 0, PIT_BURGERS = 1 };
+enum { PIT_DIRICHLET = 0, PIT_PERIODIC = 1 };           /* Eq. (2); periodic = extension */
+enum { PIT_INV_AUTO = 0, PIT_INV_RECURRENCE = 1, PIT_INV_PRODUCT_WINDOW = 2 };
+
+typedef struct {
+    int32_t abi_version;   /* must equal PIT_ABI_VERSION */
+    int32_t pde;           /* PIT_HEAT (f = g = 0) | PIT_BURGERS (f = g = u^2/2) */
+    int32_t bc;            /* PIT_DIRICHLET | PIT_PERIODIC */
+    int32_t nx, ny;        /* grid intervals; Dirichlet >= 2, periodic >= 3 */
+    int32_t nt;            /* BDF1 levels, >= 1 */
+    double  x0, x1, y0, y1;/* domain [x0,x1] x [y0,y1]; h_x = (x1-x0)/nx */
+    double  dt;            /* uniform time step tau > 0 */
+    double  m0, m2;        /* mu(u) = m0 + m2 u^2, m0, m2 >= 0 (paper heat: 0, mu0; Burgers: mu0, 0) */
+    double  newton_tol;    /* stop on max|dU_k| <= newton_tol (> 0; BASELINE: 1e-12) */
+    int32_t newton_max;    /* max Newton iterations (1..256) */
+    double  lin_rtol;      /* per-level solve: ||b~ - A~ x||_2 <= lin_rtol ||b~||_2 (A~ = diag-scaled A_n);
+                              0 = default 1e-13 */
+    double  lin_atol;      /* absolute floor on that residual; 0 = default 1e-4 * newton_tol */
+    int32_t lin_max;       /* per-level BiCGSTAB iteration cap; 0 = default 1000 */
+    int32_t inverse_mode;  /* PIT_INV_*; AUTO = recurrence unless the product window admits all levels */
+    int32_t window;        /* product-form window length; 0 = auto from the Section 7 gate */
+    int32_t pipeline_depth;/* Newton iterations in flight in the level wavefront; 0 = auto */
+    int32_t device;        /* CUDA device ordinal */
+} pit_config;
+
+typedef struct pit_handle pit_handle;
+
+/* Fill *cfg with defaults (abi_version set, everything else zero / defaults). */
+void pit_config_init(pit_config* cfg);
+
+/* Validate cfg, select the device, allocate all device memory.  *out = NULL on failure.
+ * Errors: PIT_EINVAL (cfg NULL/invalid), PIT_ECUDA (no sm_100 device), PIT_ENOMEM. */
+int pit_create(const pit_config* cfg, pit_handle** out);
+
+/* NULL-safe.  Frees everything pit_create allocated. */
+void pit_destroy(pit_handle* h);
+
+/* Synchronous solve with HOST buffers (copies in, solves, copies out).
+ *   u0    [ns]             initial data at the unknown nodes (host)
+ *   bc    [nt][2(nx+ny)]   Dirichlet rings at t^n, or NULL = homogeneous; ignored if periodic
+ *   guess [nt][ns]         initial Newton iterate, or NULL = u0 at every level
+ *   u_out [nt][ns]         solution (written for PIT_OK, PIT_OK_FLOOR and PIT_ENOCONV)
+ *   hist  [newton_max][4]  per iteration k: { rms R(U_k), max|R(U_k)|, rms dU_k, max|dU_k| }
+ *                          (rms dU_k is the paper's "residual"); may be NULL
+ *   n_iter                 iterations performed; may be NULL
+ * Returns the solve status (PIT_OK / PIT_OK_FLOOR / PIT_ENOCONV / PIT_EBREAKDOWN) or an error. */
+int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* guess,
+              double* u_out, double* hist, int32_t* n_iter);
+
+/* Asynchronous solve on the caller's stream with DEVICE buffers (same shapes as pit_solve).
+ *   d_info [2] int32 = { n_iter, status } written on the device at the end of the solve.
+ *   cuda_stream: a cudaStream_t (NULL = legacy default stream).
+ * The return value reports only argument / launch errors; the solve status is d_info[1] once the
+ * stream work completes. */
+int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, const double* d_guess,
+                     double* d_u_out, double* d_hist, int32_t* d_info, void* cuda_stream);
+
+/* Kernel (a) on its own: the space-time Newton residual R = -G(U) of Eq. (5) for all
+ * levels of the DEVICE iterate d_U [nt][ns] (u^0 = d_u0), written to d_R [nt][ns]; optional d_diag
+ * [nt][ns] receives the diagonal of every A_n (Eq. 6), and d_norms [2] = { rms R, max|R| } (both may
+ * be NULL).  Asynchronous on cuda_stream. */
+int pit_residual_device(pit_handle* h, const double* d_U, const double* d_u0, const double* d_bc,
+                        double* d_R, double* d_diag, double* d_norms, void* cuda_stream);
+
+/* Stage (c) on its own, for tests: solve A_n x = b for ONE level n (1..nt) whose Jacobian block is
+ * taken at the device iterate d_U (level n-1 from d_U, or d_u0 when n = 1, enters only via the ring /
+ * nothing — A_n depends on u^n only).  d_b, d_x: [ns] device.  d_info [2] = { iterations, status }. */
+int pit_level_solve_device(pit_handle* h, int32_t level, const double* d_U, const double* d_bc,
+                           const double* d_b, double* d_x, int32_t* d_info, void* cuda_stream);
+
+/* Stage (b2) on its own, for tests: the literal Theorem 1 product form (recursions
+ * PAPER.md:221-230) for levels [s0, s0+L) of the device iterate: given the residuals d_R [nt][ns] and
+ * the carry d_carry [ns] (= du^{s0-1}, or NULL for zero), writes du^{s0..s0+L-1} into d_dU [L][ns].
+ * Returns PIT_ECOND if the window fails the Section 7 gate (prod ||A_i||_inf > 1e6 over the window's
+ * longest chain). */
+int pit_product_window_device(pit_handle* h, int32_t s0, int32_t L, const double* d_U, const double* d_u0,
+                              const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
+                              int32_t* d_info, void* cuda_stream);
+
+/* Number of unknowns per level and device bytes the handle holds. */
+int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
+
+/* Pipeline statistics of the last solve (host-readable after the stream completes):
+ * out[0] = wavefront steps, out[1] = total BiCGSTAB iterations summed over steps (max per step),
+ * out[2] = pipeline depth used, out[3] = grid CTAs, out[4] = kernel launches of the last solve. */
+int pit_stats(pit_handle* h, int64_t* out, int32_t n);
+
+const char* pit_strerror(int code);
+const char* pit_last_error(const pit_handle* h);
+int pit_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIT_H */

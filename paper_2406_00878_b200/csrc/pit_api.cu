@@ -1,0 +1,375 @@
+// pit_api.cu — host side of libpit: the C ABI declared in include/pit.h.
+//
+// Validation, device memory ownership, launch configuration (cooperative persistent grid sized to the
+// SM count), and the host-buffer convenience path.  No arithmetic of the method runs on the host: every
+// step of the hot path is a kernel in pit_kernels.cu.  There is no CPU fallback.
+#include "pit.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "pit_kernels.cu"
+
+using namespace pit;
+
+struct pit_handle {
+    pit_config cfg;
+    Prob P;
+    int device = 0, sms = 0, G = 0, D = 1, B = 3, occ = 1;
+    double* U = nullptr;          // [B][nt][ns]
+    double* slots = nullptr;      // [D][NVEC][ns]
+    double* part = nullptr;       // [2][G][NPART]
+    double* hpart = nullptr;      // [2][G][4]
+    GridBar* bar = nullptr;
+    double* hist = nullptr;       // [newton_max][4]
+    int* info = nullptr;          // [2]
+    long long* stats = nullptr;   // [4]
+    double* d_u0 = nullptr;       // host-path staging
+    double* d_bc = nullptr;
+    double* d_small = nullptr;    // [2 * 1024] scratch for kernel (a) partials + norms
+    long long bytes = 0;
+    long long launches = 0;
+    char err[512] = {0};
+};
+
+static int set_err(pit_handle* h, int code, const char* fmt, ...) {
+    if (h) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(h->err, sizeof(h->err), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CUDA_TRY(h, call)                                                                              \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) return set_err((h), PIT_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+// (the definitions below inherit C linkage from the extern "C" declarations in pit.h)
+
+void pit_config_init(pit_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    c->abi_version = PIT_ABI_VERSION;
+    c->x1 = 1.0;
+    c->y1 = 1.0;
+    c->newton_tol = 1e-12;
+    c->newton_max = 30;
+}
+
+int pit_abi_version(void) { return PIT_ABI_VERSION; }
+
+const char* pit_strerror(int code) {
+    switch (code) {
+        case PIT_OK: return "converged";
+        case PIT_OK_FLOOR: return "converged at the rounding floor";
+        case PIT_EINVAL: return "invalid argument";
+        case PIT_ENOMEM: return "device allocation failed";
+        case PIT_ECUDA: return "CUDA error";
+        case PIT_ENOCONV: return "Newton did not converge within newton_max";
+        case PIT_EBREAKDOWN: return "Krylov breakdown or non-finite value";
+        case PIT_ECOND: return "product-form window rejected by the Section 7 conditioning gate";
+        default: return "unknown status";
+    }
+}
+
+const char* pit_last_error(const pit_handle* h) { return h ? h->err : "null handle"; }
+
+static int validate(const pit_config* c, char* why, size_t n) {
+    if (!c) { snprintf(why, n, "cfg is NULL"); return PIT_EINVAL; }
+    if (c->abi_version != PIT_ABI_VERSION) { snprintf(why, n, "abi_version %d != %d", c->abi_version, PIT_ABI_VERSION); return PIT_EINVAL; }
+    if (c->pde != PIT_HEAT && c->pde != PIT_BURGERS) { snprintf(why, n, "pde %d", c->pde); return PIT_EINVAL; }
+    if (c->bc != PIT_DIRICHLET && c->bc != PIT_PERIODIC) { snprintf(why, n, "bc %d", c->bc); return PIT_EINVAL; }
+    const int nmin = c->bc == PIT_DIRICHLET ? 2 : 3;
+    if (c->nx < nmin || c->ny < nmin) { snprintf(why, n, "nx, ny must be >= %d", nmin); return PIT_EINVAL; }
+    if (c->nx > (1 << 20) || c->ny > (1 << 20)) { snprintf(why, n, "nx, ny too large"); return PIT_EINVAL; }
+    if (c->nt < 1) { snprintf(why, n, "nt must be >= 1"); return PIT_EINVAL; }
+    if (!(c->x1 > c->x0) || !(c->y1 > c->y0)) { snprintf(why, n, "empty domain"); return PIT_EINVAL; }
+    if (!(c->dt > 0.0) || !std::isfinite(c->dt)) { snprintf(why, n, "dt must be > 0"); return PIT_EINVAL; }
+    if (!(c->m0 >= 0.0) || !(c->m2 >= 0.0)) { snprintf(why, n, "mu = m0 + m2 u^2 needs m0, m2 >= 0 (PAPER.md:50)"); return PIT_EINVAL; }
+    if (!(c->newton_tol > 0.0)) { snprintf(why, n, "newton_tol must be > 0"); return PIT_EINVAL; }
+    if (c->newton_max < 1 || c->newton_max > MAXK) { snprintf(why, n, "newton_max must be in 1..%d", MAXK); return PIT_EINVAL; }
+    if (c->lin_rtol < 0.0 || c->lin_atol < 0.0 || c->lin_max < 0) { snprintf(why, n, "negative solver tolerance"); return PIT_EINVAL; }
+    if (c->inverse_mode < 0 || c->inverse_mode > 2) { snprintf(why, n, "inverse_mode %d", c->inverse_mode); return PIT_EINVAL; }
+    if (c->pipeline_depth < 0 || c->pipeline_depth > MAXD) { snprintf(why, n, "pipeline_depth must be in 0..%d", MAXD); return PIT_EINVAL; }
+    if (c->window < 0) { snprintf(why, n, "window < 0"); return PIT_EINVAL; }
+    return PIT_OK;
+}
+
+static void free_all(pit_handle* h) {
+    cudaFree(h->U); cudaFree(h->slots); cudaFree(h->part); cudaFree(h->hpart); cudaFree(h->bar);
+    cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
+    cudaFree(h->d_small);
+    h->U = h->slots = h->part = h->hpart = h->hist = h->d_u0 = h->d_bc = h->d_small = nullptr;
+    h->bar = nullptr; h->info = nullptr; h->stats = nullptr;
+}
+
+template <class T>
+static int dalloc(pit_handle* h, T** p, size_t count) {
+    const size_t b = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void**)p, b);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(h, PIT_ENOMEM, "cudaMalloc(%zu bytes): %s", b, cudaGetErrorString(e));
+    }
+    h->bytes += (long long)b;
+    return PIT_OK;
+}
+
+int pit_create(const pit_config* cfg, pit_handle** out) {
+    if (!out) return PIT_EINVAL;
+    *out = nullptr;
+    char why[256];
+    int rc = validate(cfg, why, sizeof(why));
+    if (rc != PIT_OK) return rc;
+    pit_handle* h = new (std::nothrow) pit_handle();
+    if (!h) return PIT_ENOMEM;
+    h->cfg = *cfg;
+    pit_config& c = h->cfg;
+    if (c.lin_rtol == 0.0) c.lin_rtol = 1e-13;
+    if (c.lin_atol == 0.0) c.lin_atol = 1e-4 * c.newton_tol;
+    if (c.lin_max == 0) c.lin_max = 1000;
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        delete h;
+        return PIT_ECUDA;
+    }
+    if (c.device < 0 || c.device >= ndev) { delete h; return PIT_EINVAL; }
+    h->device = c.device;
+    cudaDeviceProp prop;
+    if (cudaSetDevice(h->device) != cudaSuccess || cudaGetDeviceProperties(&prop, h->device) != cudaSuccess) {
+        cudaGetLastError();
+        delete h;
+        return PIT_ECUDA;
+    }
+    if (prop.major != 10 || !prop.cooperativeLaunch) {   // built for sm_100a only
+        delete h;
+        return PIT_ECUDA;
+    }
+    h->sms = prop.multiProcessorCount;
+
+    Prob& P = h->P;
+    P.pde = c.pde; P.bc = c.bc; P.nx = c.nx; P.ny = c.ny;
+    P.nxu = c.bc == PIT_DIRICHLET ? c.nx - 1 : c.nx;
+    P.nyu = c.bc == PIT_DIRICHLET ? c.ny - 1 : c.ny;
+    P.nt = c.nt;
+    P.ring_len = 2 * (c.nx + c.ny);
+    P.ns = (long long)P.nxu * P.nyu;
+    const double hx = (c.x1 - c.x0) / c.nx, hy = (c.y1 - c.y0) / c.ny;
+    P.ihx2 = 1.0 / (hx * hx); P.ihy2 = 1.0 / (hy * hy);
+    P.i2hx = 1.0 / (2.0 * hx); P.i2hy = 1.0 / (2.0 * hy);
+    P.dt = c.dt; P.m0 = c.m0; P.m2 = c.m2;
+
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_newton, BLOCK, 0) != cudaSuccess || occ < 1) {
+        cudaGetLastError();
+        delete h;
+        return PIT_ECUDA;
+    }
+    h->occ = std::min(occ, 2);
+    h->G = h->sms * h->occ;
+
+    // Pipeline depth: Newton iterations in flight.  Auto: keep the slot state (13 vectors per level)
+    // within ~96 MB so it stays L2-resident (126 MB L2), at most 8, at most newton_max.
+    const long long slot_bytes = (long long)NVEC * P.ns * 8;
+    int D = c.pipeline_depth;
+    if (D == 0) {
+        D = (int)std::max<long long>(1, (96ll << 20) / std::max<long long>(slot_bytes, 1));
+        D = std::min(D, 8);
+    }
+    D = std::min(D, c.newton_max);
+    D = std::max(D, 1);
+    h->D = D;
+    h->B = std::max(3, D);
+
+    const long long N = P.ns * P.nt;
+    if ((rc = dalloc(h, &h->U, (size_t)(h->B * N))) ||
+        (rc = dalloc(h, &h->slots, (size_t)(D * NVEC * P.ns))) ||
+        (rc = dalloc(h, &h->part, (size_t)(2 * h->G * NPART))) ||
+        (rc = dalloc(h, &h->hpart, (size_t)(2 * h->G * 4))) ||
+        (rc = dalloc(h, &h->bar, 1)) ||
+        (rc = dalloc(h, &h->hist, (size_t)(4 * c.newton_max))) ||
+        (rc = dalloc(h, &h->info, 2)) ||
+        (rc = dalloc(h, &h->stats, 4)) ||
+        (rc = dalloc(h, &h->d_u0, (size_t)P.ns)) ||
+        (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
+        (rc = dalloc(h, &h->d_small, 2 * 1024 + 2))) {
+        free_all(h);
+        delete h;
+        return rc;
+    }
+    if (cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess || cudaMemset(h->stats, 0, 4 * sizeof(long long)) != cudaSuccess) {
+        cudaGetLastError();
+        free_all(h);
+        delete h;
+        return PIT_ECUDA;
+    }
+    *out = h;
+    return PIT_OK;
+}
+
+void pit_destroy(pit_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    free_all(h);
+    delete h;
+}
+
+int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes) {
+    if (!h) return PIT_EINVAL;
+    if (ns) *ns = h->P.ns;
+    if (device_bytes) *device_bytes = h->bytes;
+    return PIT_OK;
+}
+
+static SolveParams base_params(pit_handle* h) {
+    SolveParams S;
+    std::memset(&S, 0, sizeof(S));
+    S.P = h->P;
+    S.U = h->U;
+    S.B = h->B; S.D = h->D; S.G = h->G;
+    S.slotmem = h->slots;
+    S.part = h->part;
+    S.hpart = h->hpart;
+    S.bar = h->bar;
+    S.hist = h->hist;
+    S.info = h->info;
+    S.newton_tol = h->cfg.newton_tol;
+    S.lin_rtol = h->cfg.lin_rtol;
+    S.lin_atol = h->cfg.lin_atol;
+    S.newton_max = h->cfg.newton_max;
+    S.lin_max = h->cfg.lin_max;
+    S.stats = h->stats;
+    return S;
+}
+
+static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
+    CUDA_TRY(h, cudaMemsetAsync(h->bar, 0, sizeof(GridBar), st));
+    void* args[] = {(void*)&S};
+    CUDA_TRY(h, cudaLaunchCooperativeKernel((void*)k_newton, dim3(h->G), dim3(BLOCK), args, 0, st));
+    h->launches += 1;
+    return PIT_OK;
+}
+
+static int grid_for(long long n, int sms) {
+    long long g = (n + BLOCK - 1) / BLOCK;
+    return (int)std::max<long long>(1, std::min<long long>(g, (long long)sms * 8));
+}
+
+int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, const double* d_guess, double* d_u_out,
+                     double* d_hist, int32_t* d_info, void* cuda_stream) {
+    if (!h || !d_u0 || !d_u_out) return set_err(h, PIT_EINVAL, "null argument");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    h->launches = 0;
+    const long long N = h->P.ns * h->P.nt;
+    k_init_iterate<<<grid_for(N, h->sms), BLOCK, 0, st>>>(h->P.ns, h->P.nt, d_u0, d_guess, h->U);
+    CUDA_TRY(h, cudaGetLastError());
+    h->launches += 1;
+    if (d_hist) CUDA_TRY(h, cudaMemsetAsync(d_hist, 0, sizeof(double) * 4 * h->cfg.newton_max, st));
+    SolveParams S = base_params(h);
+    S.u0 = d_u0;
+    S.ring = h->P.bc == PIT_DIRICHLET ? d_bc : nullptr;
+    S.u_out = d_u_out;
+    S.hist = d_hist ? d_hist : h->hist;
+    S.info = d_info ? (int*)d_info : h->info;
+    S.mode = 0;
+    return launch_newton(h, S, st);
+}
+
+int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* guess, double* u_out, double* hist,
+              int32_t* n_iter) {
+    if (!h || !u0 || !u_out) return set_err(h, PIT_EINVAL, "null argument");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const Prob& P = h->P;
+    const long long N = P.ns * P.nt;
+    CUDA_TRY(h, cudaMemcpy(h->d_u0, u0, sizeof(double) * P.ns, cudaMemcpyHostToDevice));
+    const bool has_bc = P.bc == PIT_DIRICHLET && bc;
+    if (has_bc) CUDA_TRY(h, cudaMemcpy(h->d_bc, bc, sizeof(double) * P.nt * P.ring_len, cudaMemcpyHostToDevice));
+    // the guess is staged straight into iterate buffer 0 (k_init_iterate then copies it in place)
+    if (guess) CUDA_TRY(h, cudaMemcpy(h->U, guess, sizeof(double) * N, cudaMemcpyHostToDevice));
+    h->launches = 0;
+    k_init_iterate<<<grid_for(N, h->sms), BLOCK, 0, 0>>>(P.ns, P.nt, h->d_u0, guess ? h->U : nullptr, h->U);
+    CUDA_TRY(h, cudaGetLastError());
+    h->launches += 1;
+    CUDA_TRY(h, cudaMemset(h->hist, 0, sizeof(double) * 4 * h->cfg.newton_max));
+    SolveParams S = base_params(h);
+    S.u0 = h->d_u0;
+    S.ring = has_bc ? h->d_bc : nullptr;
+    S.u_out = nullptr;       // the host copy is taken straight from the final iterate buffer
+    S.mode = 0;
+    int rc = launch_newton(h, S, 0);
+    if (rc != PIT_OK) return rc;
+    int info[2];
+    CUDA_TRY(h, cudaMemcpy(info, h->info, sizeof(info), cudaMemcpyDeviceToHost));
+    const int kf = info[0];
+    CUDA_TRY(h, cudaMemcpy(u_out, h->U + (long long)(kf % h->B) * N, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    if (hist) CUDA_TRY(h, cudaMemcpy(hist, h->hist, sizeof(double) * 4 * h->cfg.newton_max, cudaMemcpyDeviceToHost));
+    if (n_iter) *n_iter = kf;
+    return info[1];
+}
+
+int pit_residual_device(pit_handle* h, const double* d_U, const double* d_u0, const double* d_bc, double* d_R,
+                        double* d_diag, double* d_norms, void* cuda_stream) {
+    if (!h || !d_U || !d_u0 || !d_R) return set_err(h, PIT_EINVAL, "null argument");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const long long N = h->P.ns * h->P.nt;
+    const int grid = std::min(grid_for(N, h->sms), 1024);
+    k_resjac<<<grid, BLOCK, 0, st>>>(h->P, d_U, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_R, d_diag, h->d_small);
+    CUDA_TRY(h, cudaGetLastError());
+    if (d_norms) {
+        k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, grid, N, d_norms);
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    return PIT_OK;
+}
+
+int pit_level_solve_device(pit_handle* h, int32_t level, const double* d_U, const double* d_bc, const double* d_b,
+                           double* d_x, int32_t* d_info, void* cuda_stream) {
+    if (!h || !d_U || !d_b || !d_x) return set_err(h, PIT_EINVAL, "null argument");
+    if (level < 1 || level > h->P.nt) return set_err(h, PIT_EINVAL, "level %d out of 1..%d", level, h->P.nt);
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    SolveParams S = base_params(h);
+    S.U = const_cast<double*>(d_U) + (long long)(level - 1) * h->P.ns;
+    S.u0 = S.U;
+    S.ring = h->P.bc == PIT_DIRICHLET ? d_bc : nullptr;
+    S.mode = 1;
+    S.level = level;
+    S.b_in = d_b;
+    S.x_out = d_x;
+    S.info = d_info ? (int*)d_info : h->info;
+    S.D = 1;
+    return launch_newton(h, S, st);
+}
+
+int pit_product_window_device(pit_handle* h, int32_t s0, int32_t L, const double* d_U, const double* d_u0,
+                              const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
+                              int32_t* d_info, void* cuda_stream) {
+    (void)s0; (void)L; (void)d_U; (void)d_u0; (void)d_bc; (void)d_R; (void)d_carry; (void)d_dU; (void)d_info;
+    (void)cuda_stream;
+    return set_err(h, PIT_EINVAL, "product-form window not built yet");
+}
+
+int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
+    if (!h || !out || n < 1) return PIT_EINVAL;
+    long long s[4] = {0, 0, 0, 0};
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    CUDA_TRY(h, cudaMemcpy(s, h->stats, sizeof(s), cudaMemcpyDeviceToHost));
+    const long long v[5] = {s[0], s[1], h->D, h->G, h->launches};
+    for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+    return PIT_OK;
+}
+
