@@ -1,0 +1,286 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the all-at-once BDF1 Newton hot path on B200 (BASELINE.json metric).
+
+One "step" = one full pass of the hot path over one synthetic input: pit_solve_device runs every
+Newton iteration (kernel a fused residual/Jacobian, stage b level recurrence, stage c batched level
+solves, stage d update + on-device stop test) until convergence.  Metric: space-time DOF x Newton
+iterations / s, plus achieved HBM GB/s of the dominant kernel against MEASURED_PEAKS.json.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl mine|reference]
+
+N > 1 (torchrun, one process per GPU): the path does not shard (replicas only),
+so every rank solves its own replica; value = all ranks' DOF x iterations / max-over-ranks time.
+--impl reference: the CPU oracle (sequential BDF1 + Newton, 1 core) on a bounded prefix of the same
+workload; rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time DOF x Newton iterations/s"
+UNIT = "DOF*it/s"
+BYTES_PER_DOF_IT = 16     # fused whole-iteration minimum, read U_k + write U_{k+1} (fp64)
+RESJAC_BYTES_PER_DOF = 24  # kernel (a): read U (8), write R (8) + diagonal (8)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        try:
+            rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        except Exception:
+            rows = []
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def oracle_sample(p, budget_s=15.0, max_levels=None):
+    """The oracle (sequential BDF1 + Newton, one core) on a bounded prefix of the workload: levels
+    1..L at full spatial size (a prefix is exact by causality).  Returns (value, levels, seconds)."""
+    from oracle import oracle as O
+    L = 1
+    done_dof_it, secs, levels = 0.0, 0.0, 0
+    while True:
+        r = O.solve_sequential(p, levels=L)
+        secs = r.seconds
+        done_dof_it = float(p.ns) * float(r.iters.sum())
+        levels = L
+        if secs >= budget_s or L >= (max_levels or p.nt):
+            break
+        per = secs / L
+        L = min(p.nt, max(L + 1, int(budget_s / max(per, 1e-9))))
+    return done_dof_it / secs, levels, secs
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2406_00878_b200 import workloads as W
+    p = W.config(args.config)
+    values, samples = [], []
+    for _ in range(args.warmup + args.steps):
+        v, L, secs = oracle_sample(p, budget_s=args.ref_budget)
+        values.append(v)
+        samples.append((L, secs))
+    vals = values[args.warmup:]
+    v = float(np.median(vals))
+    L = samples[-1][0]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median([s for _, s in samples[args.warmup:]])),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": p.name, "nt": p.nt, "grid": [p.nxu, p.nyu], "newton_tol": p.newton_tol},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"sequential BDF1+Newton, levels 1..{L} of {p.nt} at full {p.nxu}x{p.nyu} "
+                                       f"(causal prefix), single thread"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, help="BASELINE config 1..5 (default c5, the largest)")
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--depth", type=int, default=0, help="pipeline depth (0 = auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of oracle work per reference step")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2406_00878_b200 import pit, workloads as W
+
+    p = W.config(args.config)
+    s = pit.Solver(p, device=local, pipeline_depth=args.depth)
+    dev = torch.device("cuda", local)
+    d_u0 = torch.from_numpy(p.u0).to(dev)
+    d_ring = None if p.ring is None else torch.from_numpy(p.ring).to(dev)
+    d_out = torch.empty((p.nt, p.ns), dtype=torch.float64, device=dev)
+    d_hist = torch.zeros((s.cfg.newton_max, 4), dtype=torch.float64, device=dev)
+    d_info = torch.zeros(2, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        s.solve_device(d_u0, d_ring, None, d_out, d_hist, d_info, stream=stream)
+    barrier()
+    nit, status = (int(v) for v in d_info.cpu())
+    newton_ms, launches = [], 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.solve_device(d_u0, d_ring, None, d_out, d_hist, d_info, stream=stream)
+            st = s.stats()             # waits for this solve; per-kernel device time via CUDA events
+            newton_ms.append(st["newton_kernel_ms"])
+            launches += st["launches"]
+        e1.record(stream)
+        barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    nit, status = (int(v) for v in d_info.cpu())
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    dof_it = float(p.dof) * nit
+    value = ws * dof_it / (ms_per_step * 1e-3)
+
+    # kernel (a) standalone on the same field (the HBM-streaming stencil the north star names)
+    d_R = torch.empty_like(d_out)
+    d_D = torch.empty_like(d_out)
+    for _ in range(2):
+        s.residual_device(d_out, d_u0, d_ring, d_R, d_D, None, stream=stream)
+    ra0, ra1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    ra0.record(stream)
+    nra = 5
+    for _ in range(nra):
+        s.residual_device(d_out, d_u0, d_ring, d_R, d_D, None, stream=stream)
+    ra1.record(stream)
+    torch.cuda.synchronize(dev)
+    resjac_ms = ra0.elapsed_time(ra1) / nra
+    del d_R, d_D
+
+    # end to end through the public host API: pinned host input in, solution + hist out, every step
+    h_u0 = torch.from_numpy(p.u0).pin_memory()
+    h_out = torch.empty((p.nt, p.ns), dtype=torch.float64).pin_memory()
+    h_hist = torch.zeros((s.cfg.newton_max, 4), dtype=torch.float64).pin_memory()
+    nit_c = pit.C.c_int32(0)
+    L = pit.lib()
+    barrier()
+    te = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        rc = L.pit_solve(s.h, h_u0.data_ptr(), None if p.ring is None else p.ring.ctypes.data, None,
+                         h_out.data_ptr(), h_hist.data_ptr(), pit.C.addressof(nit_c))
+        assert rc in (0, 1), rc
+    e2e_s = (time.perf_counter() - te) / args.e2e_steps
+    t2 = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = ws * float(p.dof) * nit_c.value / float(t2.item())
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    peak, peak_kind = peaks()
+    t_newton = float(np.median(newton_ms)) * 1e-3
+    achieved = BYTES_PER_DOF_IT * p.dof * nit / t_newton / 1e9
+    resjac_gbs = RESJAC_BYTES_PER_DOF * p.dof / (resjac_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"c{args.config}", {}).get("k_newton_dram_bytes")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": p.name, "nt": p.nt, "grid": [p.nxu, p.nyu], "dof": p.dof, "newton_tol": p.newton_tol,
+                   "newton_iterations": nit, "status": status, "pipeline_depth": st["depth"], "grid_ctas": st["grid"],
+                   "l2": f"inputs larger than L2 (U = {p.dof * 8 / 1e9:.2f} GB per iterate buffer)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": "k_newton (persistent: a+b+c+d fused)", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "algorithmic": f"{BYTES_PER_DOF_IT} B per DOF per Newton iteration (SURVEY 8(d) fused minimum)"},
+        "kernels": {"k_newton_ms": t_newton * 1e3, "wavefront_steps": st["steps"],
+                    "bicgstab_iterations": st["inner_iterations"],
+                    "k_resjac": {"ms": resjac_ms, "GB/s": resjac_gbs, "frac": resjac_gbs / peak,
+                                 "algorithmic": f"{RESJAC_BYTES_PER_DOF} B/DOF"}},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(p.u0.nbytes + (0 if p.ring is None else p.ring.nbytes)),
+                "d2h_bytes_per_step": int(h_out.numel() * 8 + h_hist.numel() * 8), "seconds_per_step": e2e_s},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and ws >= 1:
+        v, Lv, secs = oracle_sample(p, budget_s=args.ref_budget)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"sequential BDF1+Newton, levels 1..{Lv} of {p.nt} at full "
+                                          f"{p.nxu}x{p.nyu} (causal prefix), {secs:.1f} s single thread"}
+    print(json.dumps(line), flush=True)
+    s.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

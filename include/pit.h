@@ -141,9 +141,11 @@ int pit_product_window_device(pit_handle* h, int32_t s0, int32_t L, const double
 /* Number of unknowns per level and device bytes the handle holds. */
 int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
 
-/* Pipeline statistics of the last solve (host-readable after the stream completes):
+/* Pipeline statistics of the last solve (synchronizes with it):
  * out[0] = wavefront steps, out[1] = total BiCGSTAB iterations summed over steps (max per step),
- * out[2] = pipeline depth used, out[3] = grid CTAs, out[4] = kernel launches of the last solve. */
+ * out[2] = pipeline depth used, out[3] = grid CTAs, out[4] = kernel launches of the last solve,
+ * out[5] = device time of the persistent Newton kernel of the last solve [ns] (CUDA events on the
+ * launching stream), out[6] = device time of the iterate-initialisation kernel [ns]. */
 int pit_stats(pit_handle* h, int64_t* out, int32_t n);
 
 const char* pit_strerror(int code);

@@ -35,6 +35,8 @@ struct pit_handle {
     double* d_small = nullptr;    // [2 * 1024] scratch for kernel (a) partials + norms
     long long bytes = 0;
     long long launches = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // k_init start/end, k_newton start/end
+    bool timed = false;
     char err[512] = {0};
 };
 
@@ -106,6 +108,7 @@ static int validate(const pit_config* c, char* why, size_t n) {
 }
 
 static void free_all(pit_handle* h) {
+    for (auto& e : h->ev) if (e) { cudaEventDestroy(e); e = nullptr; }
     cudaFree(h->U); cudaFree(h->slots); cudaFree(h->part); cudaFree(h->hpart); cudaFree(h->bar);
     cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
     cudaFree(h->d_small);
@@ -209,7 +212,10 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         delete h;
         return rc;
     }
-    if (cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess || cudaMemset(h->stats, 0, 4 * sizeof(long long)) != cudaSuccess) {
+    bool ev_ok = true;
+    for (auto& e : h->ev) ev_ok = ev_ok && cudaEventCreate(&e) == cudaSuccess;
+    if (!ev_ok || cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess ||
+        cudaMemset(h->stats, 0, 4 * sizeof(long long)) != cudaSuccess) {
         cudaGetLastError();
         free_all(h);
         delete h;
@@ -231,6 +237,11 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes) {
     if (ns) *ns = h->P.ns;
     if (device_bytes) *device_bytes = h->bytes;
     return PIT_OK;
+}
+
+static int grid_for(long long n, int sms) {
+    long long g = (n + BLOCK - 1) / BLOCK;
+    return (int)std::max<long long>(1, std::min<long long>(g, (long long)sms * 8));
 }
 
 static SolveParams base_params(pit_handle* h) {
@@ -257,14 +268,23 @@ static SolveParams base_params(pit_handle* h) {
 static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
     CUDA_TRY(h, cudaMemsetAsync(h->bar, 0, sizeof(GridBar), st));
     void* args[] = {(void*)&S};
+    CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
     CUDA_TRY(h, cudaLaunchCooperativeKernel((void*)k_newton, dim3(h->G), dim3(BLOCK), args, 0, st));
+    CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
     h->launches += 1;
     return PIT_OK;
 }
 
-static int grid_for(long long n, int sms) {
-    long long g = (n + BLOCK - 1) / BLOCK;
-    return (int)std::max<long long>(1, std::min<long long>(g, (long long)sms * 8));
+// k_init_iterate bracketed by events (per-kernel device time on the launching stream, for bench.py)
+static int launch_init(pit_handle* h, const double* d_u0, const double* d_guess, cudaStream_t st) {
+    const long long N = h->P.ns * h->P.nt;
+    CUDA_TRY(h, cudaEventRecord(h->ev[0], st));
+    k_init_iterate<<<grid_for(N, h->sms), BLOCK, 0, st>>>(h->P.ns, h->P.nt, d_u0, d_guess, h->U);
+    CUDA_TRY(h, cudaGetLastError());
+    CUDA_TRY(h, cudaEventRecord(h->ev[1], st));
+    h->launches += 1;
+    h->timed = true;
+    return PIT_OK;
 }
 
 int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, const double* d_guess, double* d_u_out,
@@ -273,10 +293,8 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
     CUDA_TRY(h, cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)cuda_stream;
     h->launches = 0;
-    const long long N = h->P.ns * h->P.nt;
-    k_init_iterate<<<grid_for(N, h->sms), BLOCK, 0, st>>>(h->P.ns, h->P.nt, d_u0, d_guess, h->U);
-    CUDA_TRY(h, cudaGetLastError());
-    h->launches += 1;
+    int rc = launch_init(h, d_u0, d_guess, st);
+    if (rc != PIT_OK) return rc;
     if (d_hist) CUDA_TRY(h, cudaMemsetAsync(d_hist, 0, sizeof(double) * 4 * h->cfg.newton_max, st));
     SolveParams S = base_params(h);
     S.u0 = d_u0;
@@ -300,16 +318,15 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     // the guess is staged straight into iterate buffer 0 (k_init_iterate then copies it in place)
     if (guess) CUDA_TRY(h, cudaMemcpy(h->U, guess, sizeof(double) * N, cudaMemcpyHostToDevice));
     h->launches = 0;
-    k_init_iterate<<<grid_for(N, h->sms), BLOCK, 0, 0>>>(P.ns, P.nt, h->d_u0, guess ? h->U : nullptr, h->U);
-    CUDA_TRY(h, cudaGetLastError());
-    h->launches += 1;
+    int rc = launch_init(h, h->d_u0, guess ? h->U : nullptr, 0);
+    if (rc != PIT_OK) return rc;
     CUDA_TRY(h, cudaMemset(h->hist, 0, sizeof(double) * 4 * h->cfg.newton_max));
     SolveParams S = base_params(h);
     S.u0 = h->d_u0;
     S.ring = has_bc ? h->d_bc : nullptr;
     S.u_out = nullptr;       // the host copy is taken straight from the final iterate buffer
     S.mode = 0;
-    int rc = launch_newton(h, S, 0);
+    rc = launch_newton(h, S, 0);
     if (rc != PIT_OK) return rc;
     int info[2];
     CUDA_TRY(h, cudaMemcpy(info, h->info, sizeof(info), cudaMemcpyDeviceToHost));
@@ -368,8 +385,14 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     long long s[4] = {0, 0, 0, 0};
     CUDA_TRY(h, cudaSetDevice(h->device));
     CUDA_TRY(h, cudaMemcpy(s, h->stats, sizeof(s), cudaMemcpyDeviceToHost));
-    const long long v[5] = {s[0], s[1], h->D, h->G, h->launches};
-    for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+    float t_init = 0.f, t_newton = 0.f;
+    if (h->timed) {
+        CUDA_TRY(h, cudaEventSynchronize(h->ev[3]));
+        CUDA_TRY(h, cudaEventElapsedTime(&t_init, h->ev[0], h->ev[1]));
+        CUDA_TRY(h, cudaEventElapsedTime(&t_newton, h->ev[2], h->ev[3]));
+    }
+    const long long v[7] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6)};
+    for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
     return PIT_OK;
 }
 

@@ -420,8 +420,9 @@ __global__ void __launch_bounds__(BLOCK) k_newton(SolveParams S) {
             const int kf = stop_k + 1;              // the returned iterate U_{k+1}
             const double* Uf = S.U + (long long)(kf % S.B) * P.nt * ns;
             const long long N = ns * P.nt;
-            for (long long q = (long long)g * BLOCK + threadIdx.x; q < N; q += (long long)G * BLOCK)
-                S.u_out[q] = Uf[q];
+            if (S.u_out)
+                for (long long q = (long long)g * BLOCK + threadIdx.x; q < N; q += (long long)G * BLOCK)
+                    S.u_out[q] = Uf[q];
             if (g == 0 && threadIdx.x == 0) {
                 S.info[0] = kf;
                 S.info[1] = stop_status;

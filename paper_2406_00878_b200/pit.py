@@ -157,9 +157,10 @@ class Solver:
                                                            _stream(stream)))
 
     def stats(self):
-        out = (C.c_int64 * 5)()
-        self._check(lib().pit_stats(self.h, out, 5))
-        return {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4]}
+        out = (C.c_int64 * 7)()
+        self._check(lib().pit_stats(self.h, out, 7))
+        return {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
+                "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6}
 
     def sizes(self):
         ns, b = C.c_int64(), C.c_int64()

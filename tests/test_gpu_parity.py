@@ -20,8 +20,8 @@ def _rand_problems():
     rng = np.random.default_rng(2024)
     ps = [W.config(1), W.config(2, n=24, nt=5), W.paper_heat(12, nt=4), W.paper_burgers(14, nt=3),
           W.custom("ph", W.HEAT, W.PERIODIC, 13, 9, 3, 0.01, 0.5, 0.7, u0=rng.standard_normal(117)),
-          W.custom("dh_ragged", W.HEAT, W.DIRICHLET, 38, 21, 3, 0.002, 1.0, 1.0, u0=rng.standard_normal(37 * 20),
-                   ring=rng.standard_normal((3, 2 * (38 + 21))), domain=(0.0, 1.3, -0.2, 0.5))]
+          W.custom("dh_ragged", W.HEAT, W.DIRICHLET, 38, 21, 3, 0.002, 1.0, 1.0, u0=0.3 * rng.standard_normal(37 * 20),
+                   ring=0.3 * rng.standard_normal((3, 2 * (38 + 21))), domain=(0.0, 1.3, -0.2, 0.5))]
     return ps
 
 
