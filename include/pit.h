@@ -82,6 +82,9 @@ typedef struct {
     int32_t window;        /* product-form window length; 0 = auto from the Section 7 gate */
     int32_t pipeline_depth;/* Newton iterations in flight in the level wavefront; 0 = auto */
     int32_t device;        /* CUDA device ordinal */
+    int32_t engine;        /* 0 = auto (on-chip if the level strips fit registers + shared memory),
+                              1 = global-state engine (any size), 2 = on-chip engine (PIT_EINVAL if it
+                              does not fit) */
 } pit_config;
 
 typedef struct pit_handle pit_handle;
@@ -145,7 +148,10 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * out[0] = wavefront steps, out[1] = total BiCGSTAB iterations summed over steps (max per step),
  * out[2] = pipeline depth used, out[3] = grid CTAs, out[4] = kernel launches of the last solve,
  * out[5] = device time of the persistent Newton kernel of the last solve [ns] (CUDA events on the
- * launching stream), out[6] = device time of the iterate-initialisation kernel [ns]. */
+ * launching stream), out[6] = device time of the iterate-initialisation kernel [ns], out[7] = engine
+ * (1 global-state, 2 on-chip), out[8..14] = on-chip engine cycle accounting summed over CTAs
+ * (prologue, phase 1, phase 2, epilogue, grid barriers, scalar reductions, step bookkeeping) when the
+ * environment variable PIT_TRACE was set at pit_create (zeros otherwise). */
 int pit_stats(pit_handle* h, int64_t* out, int32_t n);
 
 const char* pit_strerror(int code);

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -22,6 +23,11 @@ struct pit_handle {
     pit_config cfg;
     Prob P;
     int device = 0, sms = 0, G = 0, D = 1, B = 3, occ = 1;
+    int engine = 1;               // 1 = global-state k_newton, 2 = on-chip k_newton_onchip<ppt>
+    int ppt = 0, hmax = 0;
+    size_t smem2 = 0;
+    BarState* bs = nullptr;
+    unsigned long long* trace = nullptr;   // [7] cycle accounting when PIT_TRACE is set
     double* U = nullptr;          // [B][nt][ns]
     double* slots = nullptr;      // [D][NVEC][ns]
     double* part = nullptr;       // [2][G][NPART]
@@ -111,7 +117,8 @@ static void free_all(pit_handle* h) {
     for (auto& e : h->ev) if (e) { cudaEventDestroy(e); e = nullptr; }
     cudaFree(h->U); cudaFree(h->slots); cudaFree(h->part); cudaFree(h->hpart); cudaFree(h->bar);
     cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
-    cudaFree(h->d_small);
+    cudaFree(h->d_small); cudaFree(h->bs); cudaFree(h->trace);
+    h->bs = nullptr; h->trace = nullptr;
     h->U = h->slots = h->part = h->hpart = h->hist = h->d_u0 = h->d_bc = h->d_small = nullptr;
     h->bar = nullptr; h->info = nullptr; h->stats = nullptr;
 }
@@ -126,6 +133,25 @@ static int dalloc(pit_handle* h, T** p, size_t count) {
     }
     h->bytes += (long long)b;
     return PIT_OK;
+}
+
+static const void* onchip_fn(int ppt, bool trace) {
+    if (trace) {
+        switch (ppt) {
+            case 1: return (const void*)k_newton_onchip<1, true>;
+            case 2: return (const void*)k_newton_onchip<2, true>;
+            case 4: return (const void*)k_newton_onchip<4, true>;
+            case 8: return (const void*)k_newton_onchip<8, true>;
+            default: return (const void*)k_newton_onchip<16, true>;
+        }
+    }
+    switch (ppt) {
+        case 1: return (const void*)k_newton_onchip<1, false>;
+        case 2: return (const void*)k_newton_onchip<2, false>;
+        case 4: return (const void*)k_newton_onchip<4, false>;
+        case 8: return (const void*)k_newton_onchip<8, false>;
+        default: return (const void*)k_newton_onchip<16, false>;
+    }
 }
 
 int pit_create(const pit_config* cfg, pit_handle** out) {
@@ -174,26 +200,54 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     P.i2hx = 1.0 / (2.0 * hx); P.i2hy = 1.0 / (2.0 * hy);
     P.dt = c.dt; P.m0 = c.m0; P.m2 = c.m2;
 
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_newton, BLOCK, 0) != cudaSuccess || occ < 1) {
-        cudaGetLastError();
-        delete h;
-        return PIT_ECUDA;
+    // ---- engine selection ----
+    // On-chip engine (default): one 512-thread CTA per SM; pipeline depth D = the largest value <= 8
+    // (<= newton_max) whose level strips fit the register/shared-memory budget (PPT <= 8 points per
+    // thread, <= 200 KB shared).  Otherwise the global-state engine (any size).
+    const int Dmax = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : 8, c.newton_max));
+    if (c.engine != 1 && P.nxu <= 2 * BLOCK2 && h->sms <= 160) {
+        for (int D = Dmax; D >= 1 && h->engine != 2; --D) {
+            const int C = h->sms / D;
+            if (C < 1) continue;
+            const int hmax = (P.nyu + C - 1) / C;
+            const long long need = (long long)hmax * P.nxu;
+            int ppt = 0;
+            for (int cand : {1, 2, 4, 8, 16})
+                if (need <= (long long)cand * BLOCK2) { ppt = cand; break; }
+            if (!ppt) continue;
+            const size_t smem = (size_t)(2 * (hmax + 2) * (P.nxu + 2) + 4 * ppt * BLOCK2) * sizeof(double);
+            if (smem > 220 * 1024) continue;
+            int occ2 = 0;
+            bool ok = true;
+            for (bool tr : {false, true}) {
+                const void* fn = onchip_fn(ppt, tr);
+                ok = ok && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, BLOCK2, smem) == cudaSuccess && occ2 >= 1;
+            }
+            if (!ok) {
+                cudaGetLastError();
+                continue;
+            }
+            h->engine = 2; h->D = D; h->ppt = ppt; h->hmax = hmax; h->smem2 = smem; h->G = h->sms; h->occ = 1;
+        }
+        if (h->engine != 2 && c.engine == 2) { delete h; return PIT_EINVAL; }
     }
-    h->occ = std::min(occ, 2);
-    h->G = h->sms * h->occ;
-
-    // Pipeline depth: Newton iterations in flight.  Auto: keep the slot state (13 vectors per level)
-    // within ~96 MB so it stays L2-resident (126 MB L2), at most 8, at most newton_max.
-    const long long slot_bytes = (long long)NVEC * P.ns * 8;
-    int D = c.pipeline_depth;
-    if (D == 0) {
-        D = (int)std::max<long long>(1, (96ll << 20) / std::max<long long>(slot_bytes, 1));
-        D = std::min(D, 8);
+    if (h->engine != 2) {
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_newton, BLOCK, 0) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            delete h;
+            return PIT_ECUDA;
+        }
+        h->occ = std::min(occ, 2);
+        h->G = h->sms * h->occ;
+        // Pipeline depth: keep the slot state (13 vectors per level) within ~96 MB (L2 is 126 MB).
+        const long long slot_bytes = (long long)NVEC * P.ns * 8;
+        int D = c.pipeline_depth;
+        if (D == 0) D = (int)std::min<long long>(8, std::max<long long>(1, (96ll << 20) / std::max<long long>(slot_bytes, 1)));
+        h->D = std::max(1, std::min(D, c.newton_max));
     }
-    D = std::min(D, c.newton_max);
-    D = std::max(D, 1);
-    h->D = D;
+    const int D = h->D;
     h->B = std::max(3, D);
 
     const long long N = P.ns * P.nt;
@@ -207,7 +261,9 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         (rc = dalloc(h, &h->stats, 4)) ||
         (rc = dalloc(h, &h->d_u0, (size_t)P.ns)) ||
         (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
-        (rc = dalloc(h, &h->d_small, 2 * 1024 + 2))) {
+        (rc = dalloc(h, &h->d_small, 2 * 1024 + 2)) ||
+        (rc = dalloc(h, &h->bs, 1)) ||
+        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 7)))) {
         free_all(h);
         delete h;
         return rc;
@@ -266,10 +322,20 @@ static SolveParams base_params(pit_handle* h) {
 }
 
 static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
-    CUDA_TRY(h, cudaMemsetAsync(h->bar, 0, sizeof(GridBar), st));
     void* args[] = {(void*)&S};
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
-    CUDA_TRY(h, cudaLaunchCooperativeKernel((void*)k_newton, dim3(h->G), dim3(BLOCK), args, 0, st));
+    if (h->engine == 2) {
+        S.hmax = h->hmax;
+        S.bs = h->bs;
+        S.trace = h->trace;
+        if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 7 * sizeof(unsigned long long), st));
+        CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
+        CUDA_TRY(h, cudaLaunchCooperativeKernel(onchip_fn(h->ppt, h->trace != nullptr), dim3(h->G), dim3(BLOCK2), args,
+                                                h->smem2, st));
+    } else {
+        CUDA_TRY(h, cudaMemsetAsync(h->bar, 0, sizeof(GridBar), st));
+        CUDA_TRY(h, cudaLaunchCooperativeKernel((void*)k_newton, dim3(h->G), dim3(BLOCK), args, 0, st));
+    }
     CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
     h->launches += 1;
     return PIT_OK;
@@ -391,8 +457,12 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
         CUDA_TRY(h, cudaEventElapsedTime(&t_init, h->ev[0], h->ev[1]));
         CUDA_TRY(h, cudaEventElapsedTime(&t_newton, h->ev[2], h->ev[3]));
     }
-    const long long v[7] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6)};
-    for (int i = 0; i < n && i < 7; ++i) out[i] = v[i];
+    unsigned long long tr[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (h->trace) CUDA_TRY(h, cudaMemcpy(tr, h->trace, sizeof(tr), cudaMemcpyDeviceToHost));
+    const long long v[15] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
+                             h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
+                             (long long)tr[4], (long long)tr[5], (long long)tr[6]};
+    for (int i = 0; i < n && i < 15; ++i) out[i] = v[i];
     return PIT_OK;
 }
 

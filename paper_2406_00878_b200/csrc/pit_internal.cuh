@@ -67,6 +67,16 @@ struct SolveParams {
     int level;                   // mode 1: level n (1-based)
     const double* b_in;          // mode 1: right-hand side [ns]
     double* x_out;               // mode 1: solution [ns]
+    int hmax;                    // on-chip engine: max rows of a CTA strip
+    struct BarState* bs;         // on-chip engine: monotonic barrier state
+    unsigned long long* trace;   // optional cycle accounting [7] (nullptr = off)
+};
+
+// Grid barrier state of the on-chip engine (zeroed before every launch).
+struct BarState {
+    unsigned long long ctr[32];  // ctr[0] and ctr[16]: the two parity counters, 128 B apart
+    unsigned int err;            // sticky error bits (1 = NaN/Inf, 2 = Krylov breakdown)
+    unsigned int pad[31];
 };
 
 __host__ __device__ inline Slot slot_at(double* base, long long ns, int d) {
@@ -137,7 +147,9 @@ __device__ __forceinline__ Vals stencil_values(const Prob& P, const double* __re
 // zeroed (they belong to q, Eq. (4)).
 struct RJ { double G, aC, aE, aW, aN, aS; };
 
-__device__ __forceinline__ RJ residual_jacobian(const Prob& P, const Vals& v, const Nbr& q, double uprev) {
+// All five coefficients, no column dropping (the on-chip engine drops Dirichlet columns by giving the
+// operand zero halo values instead).
+__device__ __forceinline__ RJ residual_jacobian_raw(const Prob& P, const Vals& v, double uprev) {
     const double bE = 0.5 * (v.c + v.e), bW = 0.5 * (v.w + v.c), bN = 0.5 * (v.c + v.n), bS = 0.5 * (v.s + v.c);
     const double mE = law_mu(P, bE), mW = law_mu(P, bW), mN = law_mu(P, bN), mS = law_mu(P, bS);
     const double gE = v.e - v.c, gW = v.c - v.w, gN = v.n - v.c, gS = v.c - v.s;
@@ -148,10 +160,33 @@ __device__ __forceinline__ RJ residual_jacobian(const Prob& P, const Vals& v, co
     const double hE = 0.5 * law_dmu(P, bE) * gE, hW = 0.5 * law_dmu(P, bW) * gW;
     const double hN = 0.5 * law_dmu(P, bN) * gN, hS = 0.5 * law_dmu(P, bS) * gS;
     o.aC = 1.0 + P.dt * ((mE + mW - hE + hW) * P.ihx2 + (mN + mS - hN + hS) * P.ihy2);
-    o.aE = q.he ? P.dt * (law_df(P, v.e) * P.i2hx - (mE + hE) * P.ihx2) : 0.0;
-    o.aW = q.hw ? P.dt * (-law_df(P, v.w) * P.i2hx - (mW - hW) * P.ihx2) : 0.0;
-    o.aN = q.hn ? P.dt * (law_df(P, v.n) * P.i2hy - (mN + hN) * P.ihy2) : 0.0;
-    o.aS = q.hs ? P.dt * (-law_df(P, v.s) * P.i2hy - (mS - hS) * P.ihy2) : 0.0;
+    o.aE = P.dt * (law_df(P, v.e) * P.i2hx - (mE + hE) * P.ihx2);
+    o.aW = P.dt * (-law_df(P, v.w) * P.i2hx - (mW - hW) * P.ihx2);
+    o.aN = P.dt * (law_df(P, v.n) * P.i2hy - (mN + hN) * P.ihy2);
+    o.aS = P.dt * (-law_df(P, v.s) * P.i2hy - (mS - hS) * P.ihy2);
+    return o;
+}
+
+__device__ __forceinline__ RJ residual_jacobian(const Prob& P, const Vals& v, const Nbr& q, double uprev) {
+    RJ o = residual_jacobian_raw(P, v, uprev);
+    if (!q.he) o.aE = 0.0;
+    if (!q.hw) o.aW = 0.0;
+    if (!q.hn) o.aN = 0.0;
+    if (!q.hs) o.aS = 0.0;
+    return o;
+}
+
+// Off-diagonal coefficients only (the matvec of the on-chip engine recomputes them from u every time).
+struct Off { double e, w, n, s; };
+__device__ __forceinline__ Off offdiag(const Prob& P, const Vals& v) {
+    const double bE = 0.5 * (v.c + v.e), bW = 0.5 * (v.w + v.c), bN = 0.5 * (v.c + v.n), bS = 0.5 * (v.s + v.c);
+    const double hE = 0.5 * law_dmu(P, bE) * (v.e - v.c), hW = 0.5 * law_dmu(P, bW) * (v.c - v.w);
+    const double hN = 0.5 * law_dmu(P, bN) * (v.n - v.c), hS = 0.5 * law_dmu(P, bS) * (v.c - v.s);
+    Off o;
+    o.e = P.dt * (law_df(P, v.e) * P.i2hx - (law_mu(P, bE) + hE) * P.ihx2);
+    o.w = P.dt * (-law_df(P, v.w) * P.i2hx - (law_mu(P, bW) - hW) * P.ihx2);
+    o.n = P.dt * (law_df(P, v.n) * P.i2hy - (law_mu(P, bN) + hN) * P.ihy2);
+    o.s = P.dt * (-law_df(P, v.s) * P.i2hy - (law_mu(P, bS) - hS) * P.ihy2);
     return o;
 }
 

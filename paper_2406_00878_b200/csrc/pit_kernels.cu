@@ -439,3 +439,5 @@ __global__ void __launch_bounds__(BLOCK) k_newton(SolveParams S) {
 }
 
 }  // namespace pit
+
+#include "pit_newton_onchip.cuh"

@@ -1,0 +1,575 @@
+// pit_newton_onchip.cuh — the ON-CHIP engine of the persistent Newton kernel (included by pit_kernels.cu).
+//
+// Same method and same wavefront schedule as k_newton (see pit_kernels.cu), re-laid out so that a
+// per-level BiCGSTAB solve keeps its whole state in registers and shared memory for the duration of a
+// wavefront step:
+//   * one 256-thread CTA per SM (up to 255 registers per thread); a (level, iteration) pair owns a contiguous block of CTAs and every CTA
+//     owns a strip of whole rows [r0, r1) of that level;
+//   * per point, x, b~, r/s live in registers (PPT points per thread), p, v, t, 1/a_C in shared memory;
+//   * u^n of the strip plus one halo row above/below and one halo column left/right (Dirichlet ring
+//     or periodic wrap) is staged once per step in shared memory; the Jacobian coefficients of the
+//     matvec are recomputed from it (Burgers: one FMA each), so no coefficient array exists at all;
+//   * the matvec operand (p or s) is staged in shared memory; the two halo rows owned by neighbouring
+//     CTAs are recomputed from the 4 (resp. 2) values those CTAs published for their boundary rows
+//     before the last grid barrier, so each BiCGSTAB iteration needs exactly 2 grid barriers;
+//   * grid barrier = one red.release.gpu per CTA on a monotonic counter + ld.acquire spin (1.2 us on
+//     B200, profiles/r01_v1/microbench.txt), carrying an OR flag for the step-termination test;
+//   * a pair that converges does its epilogue (U_{k+1}^n = U_k^n + du^n, carry) in the next phase
+//     slot, overlapped with still-iterating pairs; the step ends at the first barrier where no pair is
+//     left iterating: 2 * (max BiCGSTAB iterations of the step) + 2 grid barriers per wavefront step.
+#pragma once
+
+namespace pit {
+
+constexpr int BLOCK2 = 256;
+constexpr int NWARP2 = BLOCK2 / 32;
+
+template <int NS, int NM>
+__device__ __forceinline__ void block_reduce2(double (&a)[NS + NM], double* sm) {
+    constexpr int N = NS + NM;
+    #pragma unroll
+    for (int i = 0; i < N; ++i)
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, a[i], o);
+            a[i] = i < NS ? a[i] + y : fmax(a[i], y);
+        }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0)
+        #pragma unroll
+        for (int i = 0; i < N; ++i) sm[w * N + i] = a[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        #pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s = sm[i];
+            for (int k = 1; k < NWARP2; ++k) s = i < NS ? s + sm[k * N + i] : fmax(s, sm[k * N + i]);
+            a[i] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// Grid barrier of the on-chip engine, after the sm_70+ cooperative-groups pattern (bar.sync + one
+// atom.release.gpu per CTA + ld.acquire.gpu polling + bar.sync), extended to carry an OR flag for free:
+// two 64-bit monotonic counters alternate by episode parity; a CTA adds 1 + (flag << 32), so the low
+// word counts arrivals and the high word counts flags.  Episode ep completes when the low word of
+// ctr[ep & 1] reaches (ep / 2 + 1) * G; nothing else is added to that counter until every CTA has
+// arrived at episode ep + 1, so the high word read at completion is exactly the flag count through
+// episode ep and its increment over the previous same-parity episode is this episode's flag count.
+__device__ __forceinline__ bool bar_sync(BarState* b, unsigned G, unsigned& ep, bool flag, unsigned (&hi)[2]) {
+    __shared__ unsigned s_any;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long* ctr = b->ctr + 16 * (ep & 1);
+        const unsigned long long add = 1ull | ((unsigned long long)(flag ? 1u : 0u) << 32);
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(add) : "memory");
+        const unsigned target = (ep / 2 + 1) * G;
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        } while ((unsigned)v < target);
+        const unsigned h = (unsigned)(v >> 32);
+        s_any = h != hi[ep & 1];
+        hi[ep & 1] = h;
+    }
+    ++ep;
+    __syncthreads();
+    return s_any;
+}
+
+// u at unknown (gc, gr) of level n, extended by the Dirichlet ring (Eq. 2) or the periodic wrap.
+__device__ __forceinline__ double node_ext(const Prob& P, const double* __restrict__ U, const double* __restrict__ ringn,
+                                           int gr, int gc) {
+    if (P.bc == 1) {
+        gr = gr < 0 ? gr + P.nyu : (gr >= P.nyu ? gr - P.nyu : gr);
+        gc = gc < 0 ? gc + P.nxu : (gc >= P.nxu ? gc - P.nxu : gc);
+        return __ldcg(U + (long long)gr * P.nxu + gc);
+    }
+    const bool in_r = gr >= 0 && gr < P.nyu, in_c = gc >= 0 && gc < P.nxu;
+    if (in_r && in_c) return __ldcg(U + (long long)gr * P.nxu + gc);
+    if (!ringn || (!in_r && !in_c)) return 0.0;          // corners are never used by the 5-point stencil
+    const int nxp = P.nx + 1;
+    if (gr < 0) return __ldcg(ringn + gc + 1);                         // bottom, paper node (gc+1, 0)
+    if (gr >= P.nyu) return __ldcg(ringn + nxp + gc + 1);              // top, (gc+1, ny)
+    if (gc < 0) return __ldcg(ringn + 2 * nxp + gr);                   // left, (0, gr+1)
+    return __ldcg(ringn + 2 * nxp + (P.ny - 1) + gr);                  // right, (nx, gr+1)
+}
+
+// Optional cycle accounting (S.trace != nullptr, env PIT_TRACE=1): per-CTA clock64 time per category,
+// summed over CTAs: 0 prologue, 1 phase-1 work, 2 phase-2 work, 3 epilogue, 4 grid barriers,
+// 5 scalar reductions after barriers, 6 end-of-step bookkeeping.
+#define PMARK(cat)                                                       \
+    do {                                                                 \
+        if (TRACE) {                                                     \
+            const long long t_ = clock64();                              \
+            prof[cat] += t_ - t_last;                                    \
+            t_last = t_;                                                 \
+        }                                                                \
+    } while (0)
+
+template <int PPT, bool TRACE>
+__global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
+    static_assert(BLOCK2 * NPART >= 4 * MAXD, "pair results live in red[]");
+    extern __shared__ double smem[];
+    const Prob P = S.P;
+    const long long ns = P.ns;
+    const int nxu = P.nxu, nyu = P.nyu;
+    const int G = S.G, g = blockIdx.x, tid = threadIdx.x;
+    const int W = nxu + 2;                         // shared row pitch: halo column each side
+    const int HR = S.hmax + 2;                     // shared rows: halo row each side
+    double* u_s = smem;                            // [HR][W]  u^n_k of the strip (+ halo / ring)
+    double* op_s = u_s + HR * W;                   // [HR][W]  matvec operand
+    double* p_s = op_s + HR * W;                   // [PPT][BLOCK2]
+    double* v_s = p_s + PPT * BLOCK2;
+    double* ci_s = v_s + PPT * BLOCK2;             // 1 / a_C
+    double* t_s = ci_s + PPT * BLOCK2;             // t = A s (lives from phase 2 to the next phase 1)
+    __shared__ int sS[MAXK];
+    __shared__ double red[NWARP2 * NPART];
+    __shared__ double s_hp_big[4 * 160];          // end-of-step norm partials of all CTAs (G <= 160)
+    __shared__ double pr[NPART];
+    __shared__ double hacc[MAXD][4];
+    __shared__ double prevmax_s;
+    if (tid == 0) {
+        const int D = S.D;
+        for (int k = 0; k < S.newton_max; ++k) {
+            int st = k == 0 ? 1 : sS[k - 1] + 1;
+            if (k >= D && sS[k - D] + P.nt > st) st = sS[k - D] + P.nt;
+            sS[k] = st;
+        }
+        prevmax_s = INFINITY;
+    }
+    if (tid < MAXD * 4) hacc[tid / 4][tid % 4] = 0.0;
+    __syncthreads();
+
+    unsigned ep = 0;
+    unsigned hi[2] = {0u, 0u};                    // thread 0: flag counts seen at the last barriers
+    long long prof[7] = {0, 0, 0, 0, 0, 0, 0};
+    long long t_last = clock64();
+    auto flush_prof = [&]() {
+        if (TRACE && tid == 0)
+            for (int j = 0; j < 7; ++j) atomicAdd(S.trace + j, (unsigned long long)prof[j]);
+    };
+    const int newton_max = S.mode == 0 ? S.newton_max : 1;
+    int set = 0, klo = 0, last_done = -1;
+    long long total_inner = 0;
+    const double rtol2 = S.lin_rtol * S.lin_rtol, atol2 = S.lin_atol * S.lin_atol;
+
+    for (int step = 1;; ++step) {
+        while (klo < newton_max && step > sS[klo] + P.nt - 1) ++klo;
+        int ks[MAXD];
+        int A = 0;
+        for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ks[A++] = k;
+        if (S.mode == 1) { A = 1; ks[0] = 0; }
+        int me = 0;
+        while (me + 1 < A && (long long)(me + 1) * G / A <= g) ++me;
+        const int g0 = (int)((long long)me * G / A), g1 = (int)((long long)(me + 1) * G / A);
+        const int kme = ks[me];
+        const int n = S.mode == 1 ? S.level : step - sS[kme] + 1;
+        const int slot = kme % S.D;
+        const int buf = kme % S.B, nbuf = (kme + 1) % S.B;
+        const Slot sl = slot_at(S.slotmem, ns, slot);
+        // published boundary-row values (full-level arrays, only strip boundary rows are touched)
+        double* const pBT = sl.bt;  double* const pX = sl.x;
+        double* const pS = sl.s;    double* const pT = sl.t;  double* const pP = sl.p[0];  double* const pV = sl.v[0];
+        double* const pR = sl.r;    double* const pV2 = sl.v[1];
+        const int c = g - g0, C = g1 - g0;
+        const int r0 = (int)((long long)c * nyu / C), r1 = (int)((long long)(c + 1) * nyu / C);
+        const int h = r1 - r0, npts = h * nxu;
+        const double* Ulev = S.mode == 1 ? S.U : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
+        const double* uprev = n == 1 ? S.u0 : Ulev - ns;
+        const double* ringn = S.ring ? S.ring + (long long)(n - 1) * P.ring_len : nullptr;
+        double* Unew = S.mode == 1 ? nullptr : S.U + ((long long)nbuf * P.nt + (n - 1)) * ns;
+        double* hp = S.hpart + (long long)(step & 1) * G * 4;
+        const bool top_valid = P.bc == 1 || r0 > 0, bot_valid = P.bc == 1 || r1 < nyu;
+        const int top_row = r0 == 0 ? nyu - 1 : r0 - 1, bot_row = r1 == nyu ? 0 : r1;
+
+        double x[PPT], bt[PPT], sr[PPT];
+
+        // ---- prologue: stage u, fused residual + Jacobian diagonal (kernel a), carry, scaling ----
+        for (int idx = tid; idx < (h + 2) * W; idx += BLOCK2) {
+            const int srow = idx / W, scol = idx - srow * W;
+            u_s[idx] = h > 0 ? node_ext(P, Ulev, ringn, r0 - 1 + srow, scol - 1) : 0.0;
+            op_s[idx] = 0.0;                      // Dirichlet halo of the operand stays 0 (dropped columns)
+        }
+        __syncthreads();
+        {
+            double a[3] = {0.0, 0.0, 0.0};       // sum bt^2, sum r^2 | max |r|
+            #pragma unroll
+            for (int m = 0; m < PPT; ++m) {
+                const int l = tid + m * BLOCK2;
+                x[m] = 0.0; bt[m] = 0.0; sr[m] = 0.0;
+                if (l < npts) {
+                    const int lr = l / nxu, lc = l - lr * nxu;
+                    const int c0 = (lr + 1) * W + lc + 1;
+                    const long long q = (long long)(r0 + lr) * nxu + lc;
+                    const Vals v = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
+                    const RJ o = residual_jacobian_raw(P, v, S.mode == 1 ? 0.0 : __ldcg(uprev + q));
+                    double rhs;
+                    if (S.mode == 1) {
+                        rhs = __ldcg(S.b_in + q);
+                    } else {
+                        const double r = -o.G;
+                        a[1] += r * r;
+                        a[2] = fmax(a[2], fabs(r));
+                        rhs = r + (n == 1 ? 0.0 : __ldcg(pX + q));
+                    }
+                    const double ci = 1.0 / o.aC;
+                    ci_s[m * BLOCK2 + tid] = ci;
+                    bt[m] = rhs * ci;
+                    sr[m] = bt[m];
+                    a[0] += bt[m] * bt[m];
+                    if (lr == 0 || lr == h - 1) pBT[q] = bt[m];
+                }
+            }
+            block_reduce2<2, 1>(a, red);
+            if (tid == 0) {
+                S.part[((long long)set * G + g) * NPART] = a[0];
+                hp[g * 4 + 0] = a[1];
+                hp[g * 4 + 1] = a[2];
+            }
+        }
+        PMARK(0);
+        bar_sync(S.bs, G, ep, false, hi);
+        PMARK(4);
+        double bnorm2;
+        {
+            double o[1];
+            pair_reduce<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, pr);
+            bnorm2 = o[0];
+        }
+        PMARK(5);
+        set ^= 1;
+        double rho = bnorm2, alpha = 0.0, omega = 1.0, beta = 0.0;
+        bool conv = bnorm2 <= atol2, pending = false, epi_done = false;
+        int it = 0, maxit_step = 0;
+
+        // operand halo rows + periodic halo columns, then the scaled matvec y = D^{-1} A op at own points
+        auto fill_wrap = [&]() {
+            if (P.bc == 1)
+                for (int rr = tid; rr < h + 2; rr += BLOCK2) {
+                    op_s[rr * W] = op_s[rr * W + nxu];
+                    op_s[rr * W + nxu + 1] = op_s[rr * W + 1];
+                }
+        };
+
+        for (;;) {
+            // ================= phase-1 slot: p update + v = A p  |  epilogue of converged pairs ======
+            if (!conv) {
+                double a[1] = {0.0};
+                // halo operand (2 rows owned by the neighbour CTAs): issue the L2 loads first so their
+                // latency overlaps the own-point update below (2 nxu <= 4 BLOCK2: <= 4 per thread)
+                double hq[4][4];
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int idx = tid + j * BLOCK2;
+                    hq[j][0] = hq[j][1] = hq[j][2] = hq[j][3] = 0.0;
+                    if (h > 0 && idx < 2 * nxu) {
+                        const int side = idx >= nxu, col = side ? idx - nxu : idx;
+                        if (side ? bot_valid : top_valid) {
+                            const long long q = (long long)(side ? bot_row : top_row) * nxu + col;
+                            if (it == 0) {
+                                hq[j][0] = __ldcg(pBT + q);
+                            } else {
+                                hq[j][0] = __ldcg(pS + q); hq[j][1] = __ldcg(pT + q);
+                                hq[j][2] = __ldcg(pP + q); hq[j][3] = __ldcg(pV + q);
+                            }
+                        }
+                    }
+                }
+                #pragma unroll
+                for (int m = 0; m < PPT; ++m) {
+                    const int l = tid + m * BLOCK2;
+                    if (l < npts) {
+                        const int lr = l / nxu, lc = l - lr * nxu;
+                        const int i = m * BLOCK2 + tid;
+                        double pn;
+                        if (it == 0) {
+                            pn = bt[m];
+                        } else {
+                            const double r = sr[m] - omega * t_s[i];
+                            if (pending) x[m] += alpha * p_s[i] + omega * sr[m];
+                            pn = r + beta * (p_s[i] - omega * v_s[i]);
+                            sr[m] = r;
+                        }
+                        p_s[i] = pn;
+                        op_s[(lr + 1) * W + lc + 1] = pn;
+                    }
+                }
+                pending = false;
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int idx = tid + j * BLOCK2;
+                    if (h > 0 && idx < 2 * nxu) {
+                        const int side = idx >= nxu, col = side ? idx - nxu : idx;
+                        const double val = it == 0 ? hq[j][0]
+                                                   : (hq[j][0] - omega * hq[j][1]) + beta * (hq[j][2] - omega * hq[j][3]);
+                        op_s[(side ? h + 1 : 0) * W + col + 1] = val;
+                    }
+                }
+                __syncthreads();
+                fill_wrap();
+                __syncthreads();
+                #pragma unroll
+                for (int m = 0; m < PPT; ++m) {
+                    const int l = tid + m * BLOCK2;
+                    if (l < npts) {
+                        const int lr = l / nxu, lc = l - lr * nxu;
+                        const int i = m * BLOCK2 + tid;
+                        const int c0 = (lr + 1) * W + lc + 1;
+                        const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
+                        const Off o = offdiag(P, uv);
+                        const double pn = op_s[c0];
+                        const double vv = pn + ci_s[i] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] +
+                                                          o.s * op_s[c0 - W]);
+                        v_s[i] = vv;
+                        a[0] += bt[m] * vv;
+                        if (lr == 0 || lr == h - 1) {
+                            const long long q = (long long)(r0 + lr) * nxu + lc;
+                            pR[q] = sr[m];
+                            pV2[q] = vv;
+                        }
+                    }
+                }
+                block_reduce2<1, 0>(a, red);
+                if (tid == 0) S.part[((long long)set * G + g) * NPART] = a[0];
+                PMARK(1);
+            } else if (!epi_done) {
+                // epilogue: du^n = x (+ the pending last update), U_{k+1}^n = U_k^n + du^n, carry
+                double a[3] = {0.0, 0.0, 0.0};
+                #pragma unroll
+                for (int m = 0; m < PPT; ++m) {
+                    const int l = tid + m * BLOCK2;
+                    if (l < npts) {
+                        const int lr = l / nxu, lc = l - lr * nxu;
+                        const int i = m * BLOCK2 + tid;
+                        const long long q = (long long)(r0 + lr) * nxu + lc;
+                        double dx = x[m];
+                        if (pending) dx += alpha * p_s[i] + omega * sr[m];
+                        if (S.mode == 1) S.x_out[q] = dx;
+                        else {
+                            pX[q] = dx;
+                            Unew[q] = u_s[(lr + 1) * W + lc + 1] + dx;
+                        }
+                        a[0] += dx * dx;
+                        a[1] = fmax(a[1], fabs(dx));
+                        if (!isfinite(dx)) a[2] = 1.0;
+                    }
+                }
+                block_reduce2<1, 2>(a, red);
+                if (tid == 0) {
+                    hp[g * 4 + 2] = a[0];
+                    hp[g * 4 + 3] = a[1];
+                    if (a[2] != 0.0) atomicOr(&S.bs->err, 1u);
+                }
+                epi_done = true;
+                pending = false;
+                PMARK(3);
+            }
+            const bool any = bar_sync(S.bs, G, ep, !conv, hi);
+            PMARK(4);
+            if (!any) { set ^= 1; break; }
+            double r0v = 0.0;
+            if (!conv) {
+                double o[1];
+                pair_reduce<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, pr);
+                r0v = o[0];
+            }
+            PMARK(5);
+            set ^= 1;
+            if (!conv) {
+                if (r0v == 0.0 || !isfinite(r0v)) {
+                    if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                    conv = true;
+                } else {
+                    alpha = rho / r0v;
+                }
+            }
+            // ================= phase 2: s = r - alpha v, t = A s ====================================
+            if (!conv) {
+                double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // (t,s) (t,t) (b~,s) (b~,t) (s,s)
+                double hq[4][2];
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int idx = tid + j * BLOCK2;
+                    hq[j][0] = hq[j][1] = 0.0;
+                    if (h > 0 && idx < 2 * nxu) {
+                        const int side = idx >= nxu, col = side ? idx - nxu : idx;
+                        if (side ? bot_valid : top_valid) {
+                            const long long q = (long long)(side ? bot_row : top_row) * nxu + col;
+                            hq[j][0] = __ldcg(pR + q); hq[j][1] = __ldcg(pV2 + q);
+                        }
+                    }
+                }
+                #pragma unroll
+                for (int m = 0; m < PPT; ++m) {
+                    const int l = tid + m * BLOCK2;
+                    if (l < npts) {
+                        const int lr = l / nxu, lc = l - lr * nxu;
+                        const double s = sr[m] - alpha * v_s[m * BLOCK2 + tid];
+                        sr[m] = s;
+                        op_s[(lr + 1) * W + lc + 1] = s;
+                    }
+                }
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int idx = tid + j * BLOCK2;
+                    if (h > 0 && idx < 2 * nxu) {
+                        const int side = idx >= nxu, col = side ? idx - nxu : idx;
+                        op_s[(side ? h + 1 : 0) * W + col + 1] = hq[j][0] - alpha * hq[j][1];
+                    }
+                }
+                __syncthreads();
+                fill_wrap();
+                __syncthreads();
+                #pragma unroll
+                for (int m = 0; m < PPT; ++m) {
+                    const int l = tid + m * BLOCK2;
+                    if (l < npts) {
+                        const int lr = l / nxu, lc = l - lr * nxu;
+                        const int i = m * BLOCK2 + tid;
+                        const int c0 = (lr + 1) * W + lc + 1;
+                        const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
+                        const Off o = offdiag(P, uv);
+                        const double s = sr[m];
+                        const double t = s + ci_s[i] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] +
+                                                        o.s * op_s[c0 - W]);
+                        t_s[i] = t;
+                        a[0] += t * s; a[1] += t * t; a[2] += bt[m] * s; a[3] += bt[m] * t; a[4] += s * s;
+                        if (lr == 0 || lr == h - 1) {
+                            const long long q = (long long)(r0 + lr) * nxu + lc;
+                            pS[q] = s; pT[q] = t; pP[q] = p_s[i]; pV[q] = v_s[i];
+                        }
+                    }
+                }
+                block_reduce2<5, 0>(a, red);
+                if (tid == 0) {
+                    double* pp = S.part + ((long long)set * G + g) * NPART;
+                    for (int j = 0; j < 5; ++j) pp[j] = a[j];
+                }
+                PMARK(2);
+            }
+            bar_sync(S.bs, G, ep, false, hi);
+            PMARK(4);
+            if (!conv) {
+                double o[5];
+                pair_reduce<5, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, pr);
+                const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];
+                ++it;
+                pending = true;
+                if (tt2 == 0.0) {
+                    omega = 0.0;
+                    conv = true;
+                } else {
+                    omega = ts / tt2;
+                    const double rhon = r0s - omega * r0t;
+                    const double rn2 = fmax(ss - 2.0 * omega * ts + omega * omega * tt2, 0.0);
+                    if (!isfinite(omega) || !isfinite(rn2)) {
+                        if (tid == 0 && c == 0) atomicOr(&S.bs->err, 1u);
+                        conv = true;
+                    } else if (rn2 <= rtol2 * bnorm2 || rn2 <= atol2 || it >= S.lin_max) {
+                        conv = true;
+                    } else if (omega == 0.0 || rhon == 0.0) {
+                        if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                        conv = true;
+                    } else {
+                        beta = (rhon / rho) * (alpha / omega);
+                        rho = rhon;
+                    }
+                }
+            }
+            set ^= 1;
+            maxit_step = it > maxit_step ? it : maxit_step;
+            PMARK(5);
+        }
+        // the epilogue of a pair that was converged from the start happened in the first phase slot
+
+        // ---- norms of the finished levels -> per-iteration accumulators; stop rule (as k_newton) ----
+        const unsigned err = *((volatile unsigned*)&S.bs->err);
+        int stop_status = 2, stop_k = -1;
+        // one round trip: all CTAs' norm partials -> shared, then one warp per pair reduces its range
+        {
+            double* s_hp = red;                              // G * 4 doubles fit? (G <= 160 -> 640)
+            for (int j = tid; j < G * 4; j += BLOCK2) s_hp_big[j] = __ldcg(hp + j);
+            __syncthreads();
+            const int w = tid >> 5, lane = tid & 31;
+            if (w < A) {
+                const int ga0 = (int)((long long)w * G / A), ga1 = (int)((long long)(w + 1) * G / A);
+                double a4[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int gg = ga0 + lane; gg < ga1; gg += 32) {
+                    a4[0] += s_hp_big[gg * 4 + 0]; a4[1] = fmax(a4[1], s_hp_big[gg * 4 + 1]);
+                    a4[2] += s_hp_big[gg * 4 + 2]; a4[3] = fmax(a4[3], s_hp_big[gg * 4 + 3]);
+                }
+                #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    a4[0] += __shfl_xor_sync(0xffffffffu, a4[0], o);
+                    a4[1] = fmax(a4[1], __shfl_xor_sync(0xffffffffu, a4[1], o));
+                    a4[2] += __shfl_xor_sync(0xffffffffu, a4[2], o);
+                    a4[3] = fmax(a4[3], __shfl_xor_sync(0xffffffffu, a4[3], o));
+                }
+                if (lane == 0) for (int j = 0; j < 4; ++j) s_hp[w * 4 + j] = a4[j];
+            }
+            __syncthreads();
+            (void)s_hp;
+        }
+        for (int a = 0; a < A; ++a) {
+            const double o[4] = {red[a * 4 + 0], red[a * 4 + 1], red[a * 4 + 2], red[a * 4 + 3]};
+            const int k = ks[a];
+            const int na = S.mode == 1 ? 1 : step - sS[k] + 1;
+            const int sa = k % S.D;
+            if (tid == 0) {
+                if (na == 1) { hacc[sa][0] = hacc[sa][1] = hacc[sa][2] = hacc[sa][3] = 0.0; }
+                hacc[sa][0] += o[0]; hacc[sa][1] = fmax(hacc[sa][1], o[1]);
+                hacc[sa][2] += o[2]; hacc[sa][3] = fmax(hacc[sa][3], o[3]);
+            }
+            __syncthreads();
+            if (S.mode == 0 && na == P.nt) {
+                last_done = k;
+                const double Ntot = (double)ns * (double)P.nt;
+                const double dmax = hacc[sa][3];
+                if (g == 0 && tid == 0) {
+                    S.hist[4 * k + 0] = sqrt(hacc[sa][0] / Ntot);
+                    S.hist[4 * k + 1] = hacc[sa][1];
+                    S.hist[4 * k + 2] = sqrt(hacc[sa][2] / Ntot);
+                    S.hist[4 * k + 3] = dmax;
+                }
+                if (dmax <= S.newton_tol) { stop_status = 0; stop_k = k; }
+                else if (k >= 1 && dmax > 0.5 * prevmax_s && dmax <= 1e3 * S.newton_tol) { stop_status = 1; stop_k = k; }
+                else if (k + 1 >= newton_max) { stop_status = -4; stop_k = k; }
+                __syncthreads();
+                if (tid == 0) prevmax_s = dmax;
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+        if (g == 0 && tid == 0) total_inner += maxit_step;
+        PMARK(6);
+        if (S.mode == 1) {
+            if (g == 0 && tid == 0) {
+                S.info[0] = maxit_step;
+                S.info[1] = err ? -5 : 0;
+            }
+            flush_prof();
+            return;
+        }
+        if (err && stop_status == 2) { stop_status = -5; stop_k = last_done; }
+        if (stop_status != 2) {
+            const int kf = stop_k + 1;
+            const double* Uf = S.U + (long long)(kf % S.B) * P.nt * ns;
+            const long long N = ns * P.nt;
+            if (S.u_out)
+                for (long long q = (long long)g * BLOCK2 + tid; q < N; q += (long long)G * BLOCK2) S.u_out[q] = __ldcg(Uf + q);
+            if (g == 0 && tid == 0) {
+                S.info[0] = kf;
+                S.info[1] = stop_status;
+                if (S.stats) { S.stats[0] = step; S.stats[1] = total_inner; S.stats[2] = S.D; S.stats[3] = G; }
+            }
+            flush_prof();
+            return;
+        }
+    }
+}
+
+#undef PMARK
+
+}  // namespace pit

@@ -34,7 +34,8 @@ class PitConfig(C.Structure):
                 ("y1", C.c_double), ("dt", C.c_double), ("m0", C.c_double), ("m2", C.c_double),
                 ("newton_tol", C.c_double), ("newton_max", C.c_int32), ("lin_rtol", C.c_double),
                 ("lin_atol", C.c_double), ("lin_max", C.c_int32), ("inverse_mode", C.c_int32),
-                ("window", C.c_int32), ("pipeline_depth", C.c_int32), ("device", C.c_int32)]
+                ("window", C.c_int32), ("pipeline_depth", C.c_int32), ("device", C.c_int32),
+                ("engine", C.c_int32)]
 
 
 class PitError(RuntimeError):
@@ -157,10 +158,14 @@ class Solver:
                                                            _stream(stream)))
 
     def stats(self):
-        out = (C.c_int64 * 7)()
-        self._check(lib().pit_stats(self.h, out, 7))
-        return {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
-                "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6}
+        out = (C.c_int64 * 15)()
+        self._check(lib().pit_stats(self.h, out, 15))
+        d = {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
+             "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6, "engine": out[7]}
+        if any(out[8:15]):
+            names = ["prologue", "phase1", "phase2", "epilogue", "barrier", "reduce", "step_tail"]
+            d["trace_cycles_per_cta"] = {k: out[8 + i] / max(1, out[3]) for i, k in enumerate(names)}
+        return d
 
     def sizes(self):
         ns, b = C.c_int64(), C.c_int64()

@@ -25,7 +25,7 @@ PREFIX = {2: 64, 3: 2, 4: 4, 5: 2}
 @pytest.mark.parametrize("c", [2, 3, 4, 5])
 def test_fullsize_config(c):
     p = W.config(c)
-    U, hist, nit, st, stats = gpu_solve(p)
+    U, hist, nit, st, stats = gpu_solve(p)      # default engine selection = what bench.py times
     assert st in (pit.PIT_OK, pit.PIT_OK_FLOOR), (st, hist)
     assert hist[-1, 3] <= 1e3 * p.newton_tol
     # (1) prefix levels against the oracle's sequential solve at full spatial size

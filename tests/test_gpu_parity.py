@@ -52,15 +52,16 @@ def test_kernel_a_residual_and_diagonal(idx):
     assert abs(norms[1] - np.abs(Ror).max()) <= 1e-14 * scale
 
 
+@pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("idx", range(6))
-def test_stage_c_level_solve_matches_lapack(idx):
+def test_stage_c_level_solve_matches_lapack(idx, engine):
     torch = torch_cuda()
     p = _rand_problems()[idx]
     rng = np.random.default_rng(50 + idx)
     U = np.tile(p.u0, (p.nt, 1)) + 0.2 * rng.standard_normal((p.nt, p.ns))
     level = p.nt
     b = rng.standard_normal(p.ns)
-    s = pit.Solver(p)
+    s = pit.Solver(p, engine=engine)
     try:
         dx = torch.empty(p.ns, dtype=torch.float64, device="cuda")
         info = torch.zeros(2, dtype=torch.int32, device="cuda")
@@ -87,12 +88,13 @@ def _parity(p, **cfg):
     return U, hist, nit, st, stats, seq
 
 
+@pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("name", ["c1", "c2_small", "c2", "paper_heat16", "paper_burgers12", "ph", "dh_ragged"])
-def test_converged_solution_matches_oracle(name):
+def test_converged_solution_matches_oracle(name, engine):
     p = {"c1": lambda: W.config(1), "c2_small": lambda: W.config(2, n=24, nt=12), "c2": lambda: W.config(2),
          "paper_heat16": lambda: W.paper_heat(16), "paper_burgers12": lambda: W.paper_burgers(12),
          "ph": lambda: _rand_problems()[4], "dh_ragged": lambda: _rand_problems()[5]}[name]()
-    U, hist, nit, st, stats, seq = _parity(p)
+    U, hist, nit, st, stats, seq = _parity(p, engine=engine)
     # the paper's accuracy tables are reproduced by the GPU path too
     if name == "paper_heat16":
         assert abs(np.abs(U - W.exact_field(p, p.exact)).max() / 1.15e-4 - 1) < 0.005
@@ -100,10 +102,11 @@ def test_converged_solution_matches_oracle(name):
         assert abs(np.abs(U - W.exact_field(p, p.exact)).mean() / 1.56e-2 - 1) < 0.005
 
 
+@pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("cfg", [1, 2])
-def test_iteration_history_matches_oracle_allatonce(cfg):
+def test_iteration_history_matches_oracle_allatonce(cfg, engine):
     p = W.config(1) if cfg == 1 else W.config(2, n=32, nt=16)
-    U, hist, nit, st, stats = gpu_solve(p)
+    U, hist, nit, st, stats = gpu_solve(p, engine=engine)
     ref = O.solve_allatonce(p, tol=p.newton_tol)
     assert nit == ref.niter and st == ref.status
     for k in range(nit):
@@ -113,22 +116,24 @@ def test_iteration_history_matches_oracle_allatonce(cfg):
     assert normwise_rel(U, ref.U) <= 1e-12
 
 
+@pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("depth", [1, 2, 3, 5, 8])
-def test_wavefront_depth_does_not_change_the_answer(depth):
+def test_wavefront_depth_does_not_change_the_answer(depth, engine):
     p = W.config(2, n=20, nt=10)
-    U1, h1, n1, s1, st1 = gpu_solve(p, pipeline_depth=1)
-    Ud, hd, nd, sd, std = gpu_solve(p, pipeline_depth=depth)
+    U1, h1, n1, s1, st1 = gpu_solve(p, pipeline_depth=1, engine=1)
+    Ud, hd, nd, sd, std = gpu_solve(p, pipeline_depth=depth, engine=engine)
     assert n1 == nd and s1 == sd
     assert normwise_rel(Ud, U1) <= 1e-13
     assert std["depth"] == min(depth, 30)
 
 
-def test_deterministic_and_host_path_identical():
+@pytest.mark.parametrize("engine", [1, 2])
+def test_deterministic_and_host_path_identical(engine):
     p = W.config(2, n=24, nt=8)
-    U1, h1, n1, s1, _ = gpu_solve(p)
-    U2, h2, n2, s2, _ = gpu_solve(p)
+    U1, h1, n1, s1, _ = gpu_solve(p, engine=engine)
+    U2, h2, n2, s2, _ = gpu_solve(p, engine=engine)
     assert np.array_equal(U1, U2) and np.array_equal(h1, h2)
-    Uh, hh, nh, sh = pit.solve(p)
+    Uh, hh, nh, sh = pit.solve(p, engine=engine)
     assert np.array_equal(Uh, U1) and nh == n1 and sh == s1
 
 
@@ -143,8 +148,9 @@ def test_nondefault_stream_and_guess():
     assert normwise_rel(U, seq.U) <= 1e-12
 
 
+@pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("case", ["nt1", "one_unknown", "periodic3", "zero_data", "constant", "linear"])
-def test_edge_cases(case):
+def test_edge_cases(case, engine):
     rng = np.random.default_rng(9)
     if case == "nt1":
         p = W.config(2, n=16, nt=1)
@@ -159,7 +165,7 @@ def test_edge_cases(case):
     else:
         p = W.config(1)
         p.m2 = 0.0
-    U, hist, nit, st, _ = gpu_solve(p)
+    U, hist, nit, st, _ = gpu_solve(p, engine=engine)
     assert st in (0, 1)
     seq = O.solve_sequential(p)
     assert np.abs(U - seq.U).max() <= 1e-10 * max(np.abs(seq.U).max(), 1e-300) or np.abs(U - seq.U).max() == 0
