@@ -24,7 +24,7 @@ struct pit_handle {
     Prob P;
     int device = 0, sms = 0, G = 0, D = 1, B = 3, occ = 1;
     int engine = 1;               // 1 = global-state k_newton, 2 = on-chip k_newton_onchip<ppt>
-    int ppt = 0, hmax = 0;
+    int ppt = 0, hmax = 0, law = 0;
     size_t smem2 = 0;
     BarState* bs = nullptr;
     unsigned long long* trace = nullptr;   // [7] cycle accounting when PIT_TRACE is set
@@ -135,23 +135,21 @@ static int dalloc(pit_handle* h, T** p, size_t count) {
     return PIT_OK;
 }
 
-static const void* onchip_fn(int ppt, bool trace) {
-    if (trace) {
-        switch (ppt) {
-            case 1: return (const void*)k_newton_onchip<1, true>;
-            case 2: return (const void*)k_newton_onchip<2, true>;
-            case 4: return (const void*)k_newton_onchip<4, true>;
-            case 8: return (const void*)k_newton_onchip<8, true>;
-            default: return (const void*)k_newton_onchip<16, true>;
-        }
-    }
+template <bool TR, int LAW>
+static const void* onchip_fn_t(int ppt) {
     switch (ppt) {
-        case 1: return (const void*)k_newton_onchip<1, false>;
-        case 2: return (const void*)k_newton_onchip<2, false>;
-        case 4: return (const void*)k_newton_onchip<4, false>;
-        case 8: return (const void*)k_newton_onchip<8, false>;
-        default: return (const void*)k_newton_onchip<16, false>;
+        case 1: return (const void*)k_newton_onchip<1, TR, LAW>;
+        case 2: return (const void*)k_newton_onchip<2, TR, LAW>;
+        case 4: return (const void*)k_newton_onchip<4, TR, LAW>;
+        case 8: return (const void*)k_newton_onchip<8, TR, LAW>;
+        default: return (const void*)k_newton_onchip<16, TR, LAW>;
     }
+}
+
+// LAW 1 = viscous Burgers with constant viscosity (m2 = 0): specialised matvec coefficients.
+static const void* onchip_fn(int ppt, bool trace, int law) {
+    if (law == 1) return trace ? onchip_fn_t<true, 1>(ppt) : onchip_fn_t<false, 1>(ppt);
+    return trace ? onchip_fn_t<true, 0>(ppt) : onchip_fn_t<false, 0>(ppt);
 }
 
 int pit_create(const pit_config* cfg, pit_handle** out) {
@@ -205,7 +203,8 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     // (<= newton_max) whose level strips fit the register/shared-memory budget (PPT <= 8 points per
     // thread, <= 200 KB shared).  Otherwise the global-state engine (any size).
     const int Dmax = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : 8, c.newton_max));
-    if (c.engine != 1 && P.nxu <= 2 * BLOCK2 && h->sms <= 160) {
+    const int law = (c.pde == PIT_BURGERS && c.m2 == 0.0) ? 1 : 0;
+    if (c.engine != 1 && P.nxu <= BLOCK2 && h->sms <= 160) {
         for (int D = Dmax; D >= 1 && h->engine != 2; --D) {
             const int C = h->sms / D;
             if (C < 1) continue;
@@ -220,7 +219,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
             int occ2 = 0;
             bool ok = true;
             for (bool tr : {false, true}) {
-                const void* fn = onchip_fn(ppt, tr);
+                const void* fn = onchip_fn(ppt, tr, law);
                 ok = ok && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
                      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, BLOCK2, smem) == cudaSuccess && occ2 >= 1;
             }
@@ -229,6 +228,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
                 continue;
             }
             h->engine = 2; h->D = D; h->ppt = ppt; h->hmax = hmax; h->smem2 = smem; h->G = h->sms; h->occ = 1;
+            h->law = law;
         }
         if (h->engine != 2 && c.engine == 2) { delete h; return PIT_EINVAL; }
     }
@@ -328,9 +328,10 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
         S.hmax = h->hmax;
         S.bs = h->bs;
         S.trace = h->trace;
+        S.x0carry = getenv("PIT_X0") ? atoi(getenv("PIT_X0")) : 1;   // default: start from du^{n-1}
         if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 7 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
-        CUDA_TRY(h, cudaLaunchCooperativeKernel(onchip_fn(h->ppt, h->trace != nullptr), dim3(h->G), dim3(BLOCK2), args,
+        CUDA_TRY(h, cudaLaunchCooperativeKernel(onchip_fn(h->ppt, h->trace != nullptr, h->law), dim3(h->G), dim3(BLOCK2), args,
                                                 h->smem2, st));
     } else {
         CUDA_TRY(h, cudaMemsetAsync(h->bar, 0, sizeof(GridBar), st));

@@ -70,6 +70,7 @@ struct SolveParams {
     int hmax;                    // on-chip engine: max rows of a CTA strip
     struct BarState* bs;         // on-chip engine: monotonic barrier state
     unsigned long long* trace;   // optional cycle accounting [7] (nullptr = off)
+    int x0carry;                 // on-chip engine: start each level solve from du^{n-1} (else 0)
 };
 
 // Grid barrier state of the on-chip engine (zeroed before every launch).

@@ -21,7 +21,7 @@
 
 namespace pit {
 
-constexpr int BLOCK2 = 256;
+constexpr int BLOCK2 = 512;
 constexpr int NWARP2 = BLOCK2 / 32;
 
 template <int NS, int NM>
@@ -48,6 +48,47 @@ __device__ __forceinline__ void block_reduce2(double (&a)[NS + NM], double* sm) 
         }
     }
     __syncthreads();
+}
+
+// Fixed-order reduction of the per-CTA partials of CTAs [g0, g1) (NS sums then NM maxima), in ONE L2
+// round trip: thread t loads CTA g0 + t's partials (C <= BLOCK2), warp 0 combines them in lane order.
+constexpr int GMAX2 = 160;                         // max CTAs (= SMs) of the on-chip engine
+
+template <int NS, int NM>
+__device__ __forceinline__ void pair_reduce2(const double* part, int stride, int g0, int g1, double (&out)[NS + NM],
+                                             double* sm /* >= GMAX2 * (NS + NM) + NS + NM */) {
+    constexpr int N = NS + NM;
+    const int C = g1 - g0;
+    if ((int)threadIdx.x < C) {
+        const double* pg = part + (long long)(g0 + threadIdx.x) * stride;
+        #pragma unroll
+        for (int i = 0; i < N; ++i) sm[i * GMAX2 + threadIdx.x] = __ldcg(pg + i);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double a[N];
+        #pragma unroll
+        for (int i = 0; i < N; ++i) a[i] = 0.0;
+        for (int t = threadIdx.x; t < C; t += 32)
+            #pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const double y = sm[i * GMAX2 + t];
+                a[i] = i < NS ? a[i] + y : fmax(a[i], y);
+            }
+        #pragma unroll
+        for (int i = 0; i < N; ++i)
+            #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double y = __shfl_xor_sync(0xffffffffu, a[i], o);
+                a[i] = i < NS ? a[i] + y : fmax(a[i], y);
+            }
+        if (threadIdx.x == 0)
+            #pragma unroll
+            for (int i = 0; i < N; ++i) sm[N * GMAX2 + i] = a[i];
+    }
+    __syncthreads();
+    #pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = sm[N * GMAX2 + i];
 }
 
 // Grid barrier of the on-chip engine, after the sm_70+ cooperative-groups pattern (bar.sync + one
@@ -108,7 +149,23 @@ __device__ __forceinline__ double node_ext(const Prob& P, const double* __restri
         }                                                                \
     } while (0)
 
-template <int PPT, bool TRACE>
+// Off-diagonal Jacobian coefficients for the matvec.  LAW 1 = viscous Burgers with constant viscosity
+// (f = g = u^2/2, mu = m0: a_E = tau (u_E / 2h - mu / h^2), ...), LAW 0 = the general law of Eq. (1).
+template <int LAW>
+__device__ __forceinline__ Off offdiag_law(const Prob& P, const Vals& v) {
+    if (LAW == 1) {
+        const double cx = P.dt * P.i2hx, cy = P.dt * P.i2hy, dx = P.dt * P.m0 * P.ihx2, dy = P.dt * P.m0 * P.ihy2;
+        Off o;
+        o.e = fma(cx, v.e, -dx);
+        o.w = fma(-cx, v.w, -dx);
+        o.n = fma(cy, v.n, -dy);
+        o.s = fma(-cy, v.s, -dy);
+        return o;
+    }
+    return offdiag(P, v);
+}
+
+template <int PPT, bool TRACE, int LAW>
 __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
     static_assert(BLOCK2 * NPART >= 4 * MAXD, "pair results live in red[]");
     extern __shared__ double smem[];
@@ -126,7 +183,8 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
     double* t_s = ci_s + PPT * BLOCK2;             // t = A s (lives from phase 2 to the next phase 1)
     __shared__ int sS[MAXK];
     __shared__ double red[NWARP2 * NPART];
-    __shared__ double s_hp_big[4 * 160];          // end-of-step norm partials of all CTAs (G <= 160)
+    __shared__ double s_hp_big[4 * GMAX2];        // end-of-step norm partials of all CTAs
+    __shared__ double s_red[5 * GMAX2 + 8];       // pair_reduce2 staging
     __shared__ double pr[NPART];
     __shared__ double hacc[MAXD][4];
     __shared__ double prevmax_s;
@@ -185,63 +243,141 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
         const int top_row = r0 == 0 ? nyu - 1 : r0 - 1, bot_row = r1 == nyu ? 0 : r1;
 
         double x[PPT], bt[PPT], sr[PPT];
+        int lrr[PPT];                              // strip-local row of point m (-1: no point)
+        #pragma unroll
+        for (int m = 0; m < PPT; ++m) {
+            const int l = tid + m * BLOCK2;
+            lrr[m] = l < npts ? l / nxu : -1;
+        }
+        const long long qbase = (long long)r0 * nxu;   // global index of point m = qbase + l
 
         // ---- prologue: stage u, fused residual + Jacobian diagonal (kernel a), carry, scaling ----
+        // u rows r0-1 .. r1 staged with cp.async (all of a thread's loads in flight at once); values
+        // outside the domain (Dirichlet ring / zero) are plain stores
         for (int idx = tid; idx < (h + 2) * W; idx += BLOCK2) {
             const int srow = idx / W, scol = idx - srow * W;
-            u_s[idx] = h > 0 ? node_ext(P, Ulev, ringn, r0 - 1 + srow, scol - 1) : 0.0;
             op_s[idx] = 0.0;                      // Dirichlet halo of the operand stays 0 (dropped columns)
+            if (h == 0) continue;
+            int gr = r0 - 1 + srow, gc = scol - 1;
+            bool inside = true;
+            if (P.bc == 1) {
+                gr = gr < 0 ? gr + nyu : (gr >= nyu ? gr - nyu : gr);
+                gc = gc < 0 ? gc + nxu : (gc >= nxu ? gc - nxu : gc);
+            } else {
+                inside = gr >= 0 && gr < nyu && gc >= 0 && gc < nxu;
+            }
+            if (inside) {
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(u_s + idx);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(Ulev + (long long)gr * nxu + gc)
+                             : "memory");
+            } else {
+                u_s[idx] = node_ext(P, Ulev, ringn, r0 - 1 + srow, scol - 1);
+            }
         }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
         __syncthreads();
+        const bool x0c = S.x0carry && S.mode == 0 && n > 1;
         {
-            double a[3] = {0.0, 0.0, 0.0};       // sum bt^2, sum r^2 | max |r|
+            double a[4] = {0.0, 0.0, 0.0, 0.0};  // sum r0^2, sum r^2, sum b~^2 | max |r|   (r0 = b~ - A~ x0)
+            // issue every global load of the thread first (u^{n-1} and the carry; b in mode 1) so their
+            // latencies overlap, then compute
+            #pragma unroll
+            for (int m = 0; m < PPT; ++m) {
+                const long long q = qbase + tid + m * BLOCK2;
+                bt[m] = 0.0; sr[m] = 0.0;
+                if (lrr[m] >= 0) {
+                    if (S.mode == 1) {
+                        sr[m] = __ldcg(S.b_in + q);
+                    } else {
+                        bt[m] = __ldcg(uprev + q);
+                        sr[m] = n == 1 ? 0.0 : __ldcg(pX + q);
+                    }
+                }
+            }
             #pragma unroll
             for (int m = 0; m < PPT; ++m) {
                 const int l = tid + m * BLOCK2;
-                x[m] = 0.0; bt[m] = 0.0; sr[m] = 0.0;
-                if (l < npts) {
-                    const int lr = l / nxu, lc = l - lr * nxu;
-                    const int c0 = (lr + 1) * W + lc + 1;
-                    const long long q = (long long)(r0 + lr) * nxu + lc;
+                x[m] = 0.0;
+                if (lrr[m] >= 0) {
+                    const int lr = lrr[m];
+                    const int c0 = l + 2 * lr + W + 1;
+                    const long long q = qbase + l;
                     const Vals v = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
-                    const RJ o = residual_jacobian_raw(P, v, S.mode == 1 ? 0.0 : __ldcg(uprev + q));
+                    const RJ o = residual_jacobian_raw(P, v, bt[m]);
                     double rhs;
                     if (S.mode == 1) {
-                        rhs = __ldcg(S.b_in + q);
+                        rhs = sr[m];
                     } else {
                         const double r = -o.G;
                         a[1] += r * r;
-                        a[2] = fmax(a[2], fabs(r));
-                        rhs = r + (n == 1 ? 0.0 : __ldcg(pX + q));
+                        a[3] = fmax(a[3], fabs(r));
+                        rhs = r + sr[m];                   // r^n + du^{n-1}  (row n of Eq. 7)
                     }
                     const double ci = 1.0 / o.aC;
-                    ci_s[m * BLOCK2 + tid] = ci;
-                    bt[m] = rhs * ci;
-                    sr[m] = bt[m];
-                    a[0] += bt[m] * bt[m];
-                    if (lr == 0 || lr == h - 1) pBT[q] = bt[m];
+                    ci_s[l] = ci;
+                    x[m] = x0c ? sr[m] : 0.0;              // initial guess: the carry du^{n-1}, or 0
+                    bt[m] = rhs * ci;                      // b~ (kept in bt until r0 is known)
+                    a[2] += bt[m] * bt[m];
+                    if (x0c) op_s[c0] = x[m];
                 }
             }
-            block_reduce2<2, 1>(a, red);
+            if (x0c) {
+                // r0 = b~ - A~ x0 with x0 = du^{n-1}: the operand halo rows are the carry of the
+                // neighbouring strips (written for every point by the previous step's epilogue)
+                for (int idx = tid; idx < 2 * nxu; idx += BLOCK2) {
+                    const int side = idx >= nxu, col = side ? idx - nxu : idx;
+                    double val = 0.0;
+                    if (h > 0 && (side ? bot_valid : top_valid))
+                        val = __ldcg(pX + (long long)(side ? bot_row : top_row) * nxu + col);
+                    op_s[(side ? h + 1 : 0) * W + col + 1] = val;
+                }
+                __syncthreads();
+                if (P.bc == 1)
+                    for (int rr = tid; rr < h + 2; rr += BLOCK2) {
+                        op_s[rr * W] = op_s[rr * W + nxu];
+                        op_s[rr * W + nxu + 1] = op_s[rr * W + 1];
+                    }
+                __syncthreads();
+            }
+            #pragma unroll
+            for (int m = 0; m < PPT; ++m) {
+                const int l = tid + m * BLOCK2;
+                if (lrr[m] >= 0) {
+                    const int lr = lrr[m];
+                    const int c0 = l + 2 * lr + W + 1;
+                    if (x0c) {
+                        const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
+                        const Off o = offdiag_law<LAW>(P, uv);
+                        bt[m] -= op_s[c0] + ci_s[l] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] +
+                                                       o.s * op_s[c0 - W]);
+                    }
+                    sr[m] = bt[m];                         // r0, and the BiCGSTAB shadow vector r^0 = r0
+                    a[0] += bt[m] * bt[m];
+                    if (lr == 0 || lr == h - 1) pBT[qbase + l] = bt[m];
+                }
+            }
+            block_reduce2<3, 1>(a, red);
             if (tid == 0) {
                 S.part[((long long)set * G + g) * NPART] = a[0];
+                S.part[((long long)set * G + g) * NPART + 1] = a[2];
                 hp[g * 4 + 0] = a[1];
-                hp[g * 4 + 1] = a[2];
+                hp[g * 4 + 1] = a[3];
             }
         }
         PMARK(0);
         bar_sync(S.bs, G, ep, false, hi);
         PMARK(4);
-        double bnorm2;
+        double bnorm2, rho;
         {
-            double o[1];
-            pair_reduce<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, pr);
-            bnorm2 = o[0];
+            double o[2];
+            pair_reduce2<2, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+            rho = o[0];                          // (r^0, r0) = ||r0||^2
+            bnorm2 = o[1];                       // ||b~||^2: reference of the relative stopping test
         }
         PMARK(5);
         set ^= 1;
-        double rho = bnorm2, alpha = 0.0, omega = 1.0, beta = 0.0;
-        bool conv = bnorm2 <= atol2, pending = false, epi_done = false;
+        double alpha = 0.0, omega = 1.0, beta = 0.0;
+        bool conv = rho <= atol2 || rho <= rtol2 * bnorm2, pending = false, epi_done = false;
         int it = 0, maxit_step = 0;
 
         // operand halo rows + periodic halo columns, then the scaled matvec y = D^{-1} A op at own points
@@ -259,9 +395,9 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 double a[1] = {0.0};
                 // halo operand (2 rows owned by the neighbour CTAs): issue the L2 loads first so their
                 // latency overlaps the own-point update below (2 nxu <= 4 BLOCK2: <= 4 per thread)
-                double hq[4][4];
+                double hq[2][4];
                 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < 2; ++j) {
                     const int idx = tid + j * BLOCK2;
                     hq[j][0] = hq[j][1] = hq[j][2] = hq[j][3] = 0.0;
                     if (h > 0 && idx < 2 * nxu) {
@@ -280,9 +416,9 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 #pragma unroll
                 for (int m = 0; m < PPT; ++m) {
                     const int l = tid + m * BLOCK2;
-                    if (l < npts) {
-                        const int lr = l / nxu, lc = l - lr * nxu;
-                        const int i = m * BLOCK2 + tid;
+                    if (lrr[m] >= 0) {
+                        const int lr = lrr[m];
+                        const int i = l;
                         double pn;
                         if (it == 0) {
                             pn = bt[m];
@@ -293,12 +429,12 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                             sr[m] = r;
                         }
                         p_s[i] = pn;
-                        op_s[(lr + 1) * W + lc + 1] = pn;
+                        op_s[l + 2 * lr + W + 1] = pn;
                     }
                 }
                 pending = false;
                 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < 2; ++j) {
                     const int idx = tid + j * BLOCK2;
                     if (h > 0 && idx < 2 * nxu) {
                         const int side = idx >= nxu, col = side ? idx - nxu : idx;
@@ -313,19 +449,19 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 #pragma unroll
                 for (int m = 0; m < PPT; ++m) {
                     const int l = tid + m * BLOCK2;
-                    if (l < npts) {
-                        const int lr = l / nxu, lc = l - lr * nxu;
-                        const int i = m * BLOCK2 + tid;
-                        const int c0 = (lr + 1) * W + lc + 1;
+                    if (lrr[m] >= 0) {
+                        const int lr = lrr[m];
+                        const int i = l;
+                        const int c0 = l + 2 * lr + W + 1;
                         const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
-                        const Off o = offdiag(P, uv);
+                        const Off o = offdiag_law<LAW>(P, uv);
                         const double pn = op_s[c0];
                         const double vv = pn + ci_s[i] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] +
                                                           o.s * op_s[c0 - W]);
                         v_s[i] = vv;
                         a[0] += bt[m] * vv;
                         if (lr == 0 || lr == h - 1) {
-                            const long long q = (long long)(r0 + lr) * nxu + lc;
+                            const long long q = qbase + l;
                             pR[q] = sr[m];
                             pV2[q] = vv;
                         }
@@ -340,16 +476,16 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 #pragma unroll
                 for (int m = 0; m < PPT; ++m) {
                     const int l = tid + m * BLOCK2;
-                    if (l < npts) {
-                        const int lr = l / nxu, lc = l - lr * nxu;
-                        const int i = m * BLOCK2 + tid;
-                        const long long q = (long long)(r0 + lr) * nxu + lc;
+                    if (lrr[m] >= 0) {
+                        const int lr = lrr[m];
+                        const int i = l;
+                        const long long q = qbase + l;
                         double dx = x[m];
                         if (pending) dx += alpha * p_s[i] + omega * sr[m];
                         if (S.mode == 1) S.x_out[q] = dx;
                         else {
                             pX[q] = dx;
-                            Unew[q] = u_s[(lr + 1) * W + lc + 1] + dx;
+                            Unew[q] = u_s[l + 2 * lr + W + 1] + dx;
                         }
                         a[0] += dx * dx;
                         a[1] = fmax(a[1], fabs(dx));
@@ -372,7 +508,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
             double r0v = 0.0;
             if (!conv) {
                 double o[1];
-                pair_reduce<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, pr);
+                pair_reduce2<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
                 r0v = o[0];
             }
             PMARK(5);
@@ -388,9 +524,9 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
             // ================= phase 2: s = r - alpha v, t = A s ====================================
             if (!conv) {
                 double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // (t,s) (t,t) (b~,s) (b~,t) (s,s)
-                double hq[4][2];
+                double hq[2][2];
                 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < 2; ++j) {
                     const int idx = tid + j * BLOCK2;
                     hq[j][0] = hq[j][1] = 0.0;
                     if (h > 0 && idx < 2 * nxu) {
@@ -404,15 +540,15 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 #pragma unroll
                 for (int m = 0; m < PPT; ++m) {
                     const int l = tid + m * BLOCK2;
-                    if (l < npts) {
-                        const int lr = l / nxu, lc = l - lr * nxu;
-                        const double s = sr[m] - alpha * v_s[m * BLOCK2 + tid];
+                    if (lrr[m] >= 0) {
+                        const int lr = lrr[m];
+                        const double s = sr[m] - alpha * v_s[l];
                         sr[m] = s;
-                        op_s[(lr + 1) * W + lc + 1] = s;
+                        op_s[l + 2 * lr + W + 1] = s;
                     }
                 }
                 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < 2; ++j) {
                     const int idx = tid + j * BLOCK2;
                     if (h > 0 && idx < 2 * nxu) {
                         const int side = idx >= nxu, col = side ? idx - nxu : idx;
@@ -425,19 +561,19 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 #pragma unroll
                 for (int m = 0; m < PPT; ++m) {
                     const int l = tid + m * BLOCK2;
-                    if (l < npts) {
-                        const int lr = l / nxu, lc = l - lr * nxu;
-                        const int i = m * BLOCK2 + tid;
-                        const int c0 = (lr + 1) * W + lc + 1;
+                    if (lrr[m] >= 0) {
+                        const int lr = lrr[m];
+                        const int i = l;
+                        const int c0 = l + 2 * lr + W + 1;
                         const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
-                        const Off o = offdiag(P, uv);
+                        const Off o = offdiag_law<LAW>(P, uv);
                         const double s = sr[m];
                         const double t = s + ci_s[i] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] +
                                                         o.s * op_s[c0 - W]);
                         t_s[i] = t;
                         a[0] += t * s; a[1] += t * t; a[2] += bt[m] * s; a[3] += bt[m] * t; a[4] += s * s;
                         if (lr == 0 || lr == h - 1) {
-                            const long long q = (long long)(r0 + lr) * nxu + lc;
+                            const long long q = qbase + l;
                             pS[q] = s; pT[q] = t; pP[q] = p_s[i]; pV[q] = v_s[i];
                         }
                     }
@@ -453,7 +589,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
             PMARK(4);
             if (!conv) {
                 double o[5];
-                pair_reduce<5, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, pr);
+                pair_reduce2<5, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
                 const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];
                 ++it;
                 pending = true;
