@@ -151,7 +151,9 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * launching stream), out[6] = device time of the iterate-initialisation kernel [ns], out[7] = engine
  * (1 global-state, 2 on-chip), out[8..14] = on-chip engine cycle accounting summed over CTAs
  * (prologue, phase 1, phase 2, epilogue, grid barriers, scalar reductions, step bookkeeping) when the
- * environment variable PIT_TRACE was set at pit_create (zeros otherwise). */
+ * environment variable PIT_TRACE was set at pit_create (zeros otherwise), out[15] = 1 if the last solve
+ * inverted Eq. (6) with the (b2) product form (inverse_mode PRODUCT_WINDOW, or AUTO with the whole horizon
+ * inside the Section 7 gate), 0 for the on-device level recurrence. */
 int pit_stats(pit_handle* h, int64_t* out, int32_t n);
 
 const char* pit_strerror(int code);

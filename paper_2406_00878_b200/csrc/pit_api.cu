@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "pit_kernels.cu"
 
@@ -28,6 +29,11 @@ struct pit_handle {
     size_t smem2 = 0;
     BarState* bs = nullptr;
     unsigned long long* trace = nullptr;   // [7] cycle accounting when PIT_TRACE is set
+    double* pf_Y = nullptr;       // (b2) product-form scratch: [2][nt][ns] chain vectors
+    double* pf_R = nullptr;       // (b2) host-driven Newton: residuals [nt][ns]
+    double* pf_dU = nullptr;      // (b2) host-driven Newton: update [nt][ns]
+    double* pf_part = nullptr;    // (b2) partials
+    bool product_used = false;    // last solve used the (b2) product-form path
     double* U = nullptr;          // [B][nt][ns]
     double* slots = nullptr;      // [D][NVEC][ns]
     double* part = nullptr;       // [2][G][NPART]
@@ -118,7 +124,8 @@ static void free_all(pit_handle* h) {
     cudaFree(h->U); cudaFree(h->slots); cudaFree(h->part); cudaFree(h->hpart); cudaFree(h->bar);
     cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
     cudaFree(h->d_small); cudaFree(h->bs); cudaFree(h->trace);
-    h->bs = nullptr; h->trace = nullptr;
+    cudaFree(h->pf_Y); cudaFree(h->pf_R); cudaFree(h->pf_dU); cudaFree(h->pf_part);
+    h->bs = nullptr; h->trace = nullptr; h->pf_Y = h->pf_R = h->pf_dU = h->pf_part = nullptr;
     h->U = h->slots = h->part = h->hpart = h->hist = h->d_u0 = h->d_bc = h->d_small = nullptr;
     h->bar = nullptr; h->info = nullptr; h->stats = nullptr;
 }
@@ -354,6 +361,91 @@ static int launch_init(pit_handle* h, const double* d_u0, const double* d_guess,
     return PIT_OK;
 }
 
+
+// (b2) helpers, defined below pit_level_solve_device
+static const double PIT_GATE = 1e6;     // prod ||A_i||_inf bound over a window's longest forward chain
+static int ensure_pf_scratch(pit_handle* h);
+static int level_anorms(pit_handle* h, const double* d_U, const double* d_bc, int n0, int L, double* out, cudaStream_t st);
+static double chain_bound(const double* anorm_from_s0, int L);
+static int product_window(pit_handle* h, int s0, int L, const double* d_U, const double* d_bc, const double* d_R,
+                          const double* d_carry, double* d_dU, int* d_info, cudaStream_t st);
+
+// Host-driven all-at-once Newton with the (b2) product-form inverse (inverse_mode PRODUCT_WINDOW): the same
+// iteration, initial guess, norms and stop rule as the persistent kernels, but Eq. (6) is inverted window by
+// window with Theorem 1 (windows chained by the exact carry).  One host round trip per Newton iteration
+// (norms); the default recurrence path has none.
+static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, double* d_u_out, double* d_hist,
+                         int* d_info, cudaStream_t st) {
+    int rc = ensure_pf_scratch(h);
+    if (rc != PIT_OK) return rc;
+    const Prob& P = h->P;
+    const long long ns = P.ns, N = ns * P.nt;
+    double* U = h->U;                             // iterate buffer 0 holds U_0 (k_init_iterate)
+    const double* ring = P.bc == PIT_DIRICHLET ? d_bc : nullptr;
+    const int kmax = h->cfg.newton_max;
+    std::vector<double> hist((size_t)4 * kmax, 0.0), an(P.nt);
+    int status = PIT_ENOCONV, kdone = 0;
+    double prevmax = INFINITY;
+    const int gr = std::min(grid_for(N, h->sms), 1024);
+    for (int k = 0; k < kmax; ++k) {
+        k_resjac<<<gr, BLOCK, 0, st>>>(P, U, d_u0, ring, h->pf_R, nullptr, h->d_small);
+        CUDA_TRY(h, cudaGetLastError());
+        k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, gr, N, h->d_small + 2048);
+        CUDA_TRY(h, cudaGetLastError());
+        double rn[2];
+        CUDA_TRY(h, cudaMemcpyAsync(rn, h->d_small + 2048, sizeof(rn), cudaMemcpyDeviceToHost, st));
+        for (int s0 = 1; s0 <= P.nt;) {
+            int L;
+            if ((rc = level_anorms(h, U, d_bc, s0, P.nt - s0 + 1, an.data(), st)) != PIT_OK) return rc;
+            if (h->cfg.window > 0) {
+                L = std::min(h->cfg.window, P.nt - s0 + 1);
+                if (!(chain_bound(an.data(), L) <= PIT_GATE))
+                    return set_err(h, PIT_ECOND, "forced window [%d, %d) fails the Section 7 gate", s0, s0 + L);
+            } else {
+                L = 1;
+                while (s0 + L <= P.nt && chain_bound(an.data(), L + 1) <= PIT_GATE) ++L;
+            }
+            rc = product_window(h, s0, L, U, d_bc, h->pf_R, s0 == 1 ? nullptr : h->pf_dU + (long long)(s0 - 2) * ns,
+                                h->pf_dU + (long long)(s0 - 1) * ns, d_info, st);
+            if (rc != PIT_OK) return rc;
+            s0 += L;
+        }
+        const int gu = std::min(grid_for(N, h->sms), 1024);
+        k_update<<<gu, BLOCK, 0, st>>>(N, U, h->pf_dU, h->pf_part);
+        CUDA_TRY(h, cudaGetLastError());
+        std::vector<double> up((size_t)3 * gu);
+        CUDA_TRY(h, cudaMemcpyAsync(up.data(), h->pf_part, up.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+        double s2 = 0.0, mx = 0.0, bad = 0.0;
+        for (int b = 0; b < gu; ++b) { s2 += up[3 * b]; mx = std::max(mx, up[3 * b + 1]); bad = std::max(bad, up[3 * b + 2]); }
+        hist[4 * k + 0] = rn[0]; hist[4 * k + 1] = rn[1];
+        hist[4 * k + 2] = std::sqrt(s2 / (double)N); hist[4 * k + 3] = mx;
+        kdone = k + 1;
+        if (bad != 0.0) { status = PIT_EBREAKDOWN; break; }
+        if (mx <= h->cfg.newton_tol) { status = PIT_OK; break; }
+        if (k >= 1 && mx > 0.5 * prevmax && mx <= 1e3 * h->cfg.newton_tol) { status = PIT_OK_FLOOR; break; }
+        prevmax = mx;
+    }
+    if (d_u_out) CUDA_TRY(h, cudaMemcpyAsync(d_u_out, U, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
+    if (d_hist) CUDA_TRY(h, cudaMemcpyAsync(d_hist, hist.data(), sizeof(double) * 4 * kmax, cudaMemcpyHostToDevice, st));
+    const int info[2] = {kdone, status};
+    CUDA_TRY(h, cudaMemcpyAsync(d_info ? d_info : h->info, info, sizeof(info), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    h->product_used = true;
+    return PIT_OK;
+}
+
+// AUTO: the paper's literal product form when the Section 7 gate admits the whole horizon as one window
+// (BASELINE c1), the recurrence otherwise.
+static bool want_product(pit_handle* h, const double* d_bc, cudaStream_t st) {
+    if (h->cfg.inverse_mode == PIT_INV_PRODUCT_WINDOW) return true;
+    if (h->cfg.inverse_mode == PIT_INV_RECURRENCE || h->P.nt > 64) return false;
+    if (ensure_pf_scratch(h) != PIT_OK) return false;
+    std::vector<double> an(h->P.nt);
+    if (level_anorms(h, h->U, d_bc, 1, h->P.nt, an.data(), st) != PIT_OK) return false;
+    return chain_bound(an.data(), h->P.nt) <= PIT_GATE;
+}
+
 int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, const double* d_guess, double* d_u_out,
                      double* d_hist, int32_t* d_info, void* cuda_stream) {
     if (!h || !d_u0 || !d_u_out) return set_err(h, PIT_EINVAL, "null argument");
@@ -363,6 +455,8 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
     int rc = launch_init(h, d_u0, d_guess, st);
     if (rc != PIT_OK) return rc;
     if (d_hist) CUDA_TRY(h, cudaMemsetAsync(d_hist, 0, sizeof(double) * 4 * h->cfg.newton_max, st));
+    h->product_used = false;
+    if (want_product(h, d_bc, st)) return solve_product(h, d_u0, d_bc, d_u_out, d_hist, (int*)d_info, st);
     SolveParams S = base_params(h);
     S.u0 = d_u0;
     S.ring = h->P.bc == PIT_DIRICHLET ? d_bc : nullptr;
@@ -388,17 +482,24 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     int rc = launch_init(h, h->d_u0, guess ? h->U : nullptr, 0);
     if (rc != PIT_OK) return rc;
     CUDA_TRY(h, cudaMemset(h->hist, 0, sizeof(double) * 4 * h->cfg.newton_max));
-    SolveParams S = base_params(h);
-    S.u0 = h->d_u0;
-    S.ring = has_bc ? h->d_bc : nullptr;
-    S.u_out = nullptr;       // the host copy is taken straight from the final iterate buffer
-    S.mode = 0;
-    rc = launch_newton(h, S, 0);
+    h->product_used = false;
+    const bool prod = want_product(h, has_bc ? h->d_bc : nullptr, 0);
+    if (prod) {
+        rc = solve_product(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
+    } else {
+        SolveParams S = base_params(h);
+        S.u0 = h->d_u0;
+        S.ring = has_bc ? h->d_bc : nullptr;
+        S.u_out = nullptr;       // the host copy is taken straight from the final iterate buffer
+        S.mode = 0;
+        rc = launch_newton(h, S, 0);
+    }
     if (rc != PIT_OK) return rc;
     int info[2];
     CUDA_TRY(h, cudaMemcpy(info, h->info, sizeof(info), cudaMemcpyDeviceToHost));
     const int kf = info[0];
-    CUDA_TRY(h, cudaMemcpy(u_out, h->U + (long long)(kf % h->B) * N, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    const double* Uf = prod ? h->U : h->U + (long long)(kf % h->B) * N;
+    CUDA_TRY(h, cudaMemcpy(u_out, Uf, sizeof(double) * N, cudaMemcpyDeviceToHost));
     if (hist) CUDA_TRY(h, cudaMemcpy(hist, h->hist, sizeof(double) * 4 * h->cfg.newton_max, cudaMemcpyDeviceToHost));
     if (n_iter) *n_iter = kf;
     return info[1];
@@ -420,31 +521,145 @@ int pit_residual_device(pit_handle* h, const double* d_U, const double* d_u0, co
     return PIT_OK;
 }
 
+// Batch of independent level solves A_{lev[a]} x_a = b_a (A at the iterate d_U [nt][ns]); chunks of <= D.
+static int level_solves(pit_handle* h, int nb, const int* lev, const double* const* b, double* const* x, const double* d_U,
+                        const double* d_bc, int* d_info, cudaStream_t st) {
+    for (int a0 = 0; a0 < nb; a0 += h->D) {
+        SolveParams S = base_params(h);
+        S.U = const_cast<double*>(d_U);
+        S.u0 = d_U;
+        S.ring = h->P.bc == PIT_DIRICHLET ? d_bc : nullptr;
+        S.mode = 1;
+        S.nb = std::min(h->D, nb - a0);
+        for (int j = 0; j < S.nb; ++j) {
+            S.blev[j] = lev[a0 + j];
+            S.bptr[j] = b[a0 + j];
+            S.xptr[j] = x[a0 + j];
+        }
+        S.info = d_info ? d_info : h->info;
+        S.x0carry = 0;
+        int rc = launch_newton(h, S, st);
+        if (rc != PIT_OK) return rc;
+    }
+    return PIT_OK;
+}
+
 int pit_level_solve_device(pit_handle* h, int32_t level, const double* d_U, const double* d_bc, const double* d_b,
                            double* d_x, int32_t* d_info, void* cuda_stream) {
     if (!h || !d_U || !d_b || !d_x) return set_err(h, PIT_EINVAL, "null argument");
     if (level < 1 || level > h->P.nt) return set_err(h, PIT_EINVAL, "level %d out of 1..%d", level, h->P.nt);
     CUDA_TRY(h, cudaSetDevice(h->device));
-    cudaStream_t st = (cudaStream_t)cuda_stream;
-    SolveParams S = base_params(h);
-    S.U = const_cast<double*>(d_U) + (long long)(level - 1) * h->P.ns;
-    S.u0 = S.U;
-    S.ring = h->P.bc == PIT_DIRICHLET ? d_bc : nullptr;
-    S.mode = 1;
-    S.level = level;
-    S.b_in = d_b;
-    S.x_out = d_x;
-    S.info = d_info ? (int*)d_info : h->info;
-    S.D = 1;
-    return launch_newton(h, S, st);
+    const int lev[1] = {level};
+    const double* b[1] = {d_b};
+    double* x[1] = {d_x};
+    return level_solves(h, 1, lev, b, x, d_U, d_bc, (int*)d_info, (cudaStream_t)cuda_stream);
+}
+
+// ---- (b2): the literal Theorem 1 product form inside a Section 7 window ------------------------------
+
+static int ensure_pf_scratch(pit_handle* h) {
+    if (h->pf_Y) return PIT_OK;
+    const long long ns = h->P.ns, N = ns * h->P.nt;
+    int rc;
+    if ((rc = dalloc(h, &h->pf_Y, (size_t)(2 * N))) || (rc = dalloc(h, &h->pf_R, (size_t)N)) ||
+        (rc = dalloc(h, &h->pf_dU, (size_t)N)) || (rc = dalloc(h, &h->pf_part, (size_t)(4096 + 8))))
+        return rc;
+    return PIT_OK;
+}
+
+// ||A_n||_inf for levels n0..n0+L-1 at d_U -> host array (synchronizes the stream).
+static int level_anorms(pit_handle* h, const double* d_U, const double* d_bc, int n0, int L, double* out, cudaStream_t st) {
+    const int gx = std::max(1, std::min(64, (int)((h->P.ns + BLOCK - 1) / BLOCK)));
+    for (int c0 = 0; c0 < L; c0 += 32) {
+        const int Lc = std::min(32, L - c0);
+        k_anorm<<<dim3(gx, Lc), BLOCK, 0, st>>>(h->P, d_U, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, n0 + c0, h->pf_part);
+        CUDA_TRY(h, cudaGetLastError());
+        std::vector<double> tmp((size_t)gx * Lc);
+        CUDA_TRY(h, cudaMemcpyAsync(tmp.data(), h->pf_part, tmp.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(h, cudaStreamSynchronize(st));
+        for (int j = 0; j < Lc; ++j) {
+            double m = 0.0;
+            for (int b = 0; b < gx; ++b) m = std::max(m, tmp[(size_t)j * gx + b]);
+            out[c0 + j] = m;
+        }
+    }
+    return PIT_OK;
+}
+
+// Longest chain of a window [s0, s0+L): P^{L-1} r^L applies A_{s0} .. A_{s0+L-2}.
+static double chain_bound(const double* anorm_from_s0, int L) {
+    double p = 1.0;
+    for (int i = 0; i + 1 < L; ++i) p *= anorm_from_s0[i];
+    return p;
+}
+
+// du^{s0..s0+L-1} of Eq. (6) by Theorem 1: y^m = A_1..A_{m-1} r^m (batched stencil chain), r~^m = sum_{j<=m} y^j
+// (level scan), then P^m du^m = r~^m solved as A_m^{-1} .. A_1^{-1} r~^m (nested multi-right-hand-side
+// level solves: at nested step q every m >= q solves with the same A_q).  Window-local A_m = A_{s0+m-1}.
+static int product_window(pit_handle* h, int s0, int L, const double* d_U, const double* d_bc, const double* d_R,
+                          const double* d_carry, double* d_dU, int* d_info, cudaStream_t st) {
+    const long long ns = h->P.ns;
+    double* Y = h->pf_Y;                       // [L][ns] chain / scan / nested-solve vectors
+    double* T = h->pf_Y + (long long)h->P.nt * ns;   // [L][ns] ping-pong partner of the chain
+    CUDA_TRY(h, cudaMemcpyAsync(Y, d_R + (long long)(s0 - 1) * ns, sizeof(double) * L * ns, cudaMemcpyDeviceToDevice, st));
+    if (d_carry) {   // first row of the window: A_{s0} du^{s0} = r^{s0} + du^{s0-1}
+        k_update<<<grid_for(ns, h->sms), BLOCK, 0, st>>>(ns, Y, d_carry, h->pf_part);   // Y[0] += carry
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    const int gx = grid_for(ns, h->sms);
+    for (int j = 1; j <= L - 1; ++j) {         // chain step j: vector m (m - 1 >= j) applies A_{m-j}
+        std::vector<int> ms;
+        for (int m = j + 1; m <= L; ++m) ms.push_back(m);
+        for (size_t c0 = 0; c0 < ms.size(); c0 += MAXD) {
+            MatvecJobs J;
+            J.n = (int)std::min<size_t>(MAXD, ms.size() - c0);
+            for (int t = 0; t < J.n; ++t) {
+                const int m = ms[c0 + t];
+                J.lev[t] = s0 + (m - j) - 1;
+                J.x[t] = Y + (long long)(m - 1) * ns;
+                J.y[t] = T + (long long)(m - 1) * ns;
+            }
+            k_matvec_batch<<<dim3(std::min(gx, 256), J.n), BLOCK, 0, st>>>(h->P, d_U, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, J);
+            CUDA_TRY(h, cudaGetLastError());
+        }
+        // move the chained vectors back into Y
+        CUDA_TRY(h, cudaMemcpyAsync(Y + (long long)j * ns, T + (long long)j * ns, sizeof(double) * (L - j) * ns,
+                                    cudaMemcpyDeviceToDevice, st));
+    }
+    k_level_prefix<<<gx, BLOCK, 0, st>>>(ns, L, Y);
+    CUDA_TRY(h, cudaGetLastError());
+    for (int q = 1; q <= L; ++q) {             // nested step q: every m >= q solves A_q z = z
+        std::vector<int> lev;
+        std::vector<const double*> b;
+        std::vector<double*> x;
+        for (int m = q; m <= L; ++m) {
+            lev.push_back(s0 + q - 1);
+            b.push_back(Y + (long long)(m - 1) * ns);
+            x.push_back(Y + (long long)(m - 1) * ns);
+        }
+        int rc = level_solves(h, (int)lev.size(), lev.data(), b.data(), x.data(), d_U, d_bc, d_info, st);
+        if (rc != PIT_OK) return rc;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(d_dU, Y, sizeof(double) * L * ns, cudaMemcpyDeviceToDevice, st));
+    return PIT_OK;
 }
 
 int pit_product_window_device(pit_handle* h, int32_t s0, int32_t L, const double* d_U, const double* d_u0,
                               const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
                               int32_t* d_info, void* cuda_stream) {
-    (void)s0; (void)L; (void)d_U; (void)d_u0; (void)d_bc; (void)d_R; (void)d_carry; (void)d_dU; (void)d_info;
-    (void)cuda_stream;
-    return set_err(h, PIT_EINVAL, "product-form window not built yet");
+    (void)d_u0;
+    if (!h || !d_U || !d_R || !d_dU) return set_err(h, PIT_EINVAL, "null argument");
+    if (s0 < 1 || L < 1 || s0 + L - 1 > h->P.nt) return set_err(h, PIT_EINVAL, "window [%d, %d) out of 1..%d", s0, s0 + L, h->P.nt);
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int rc = ensure_pf_scratch(h);
+    if (rc != PIT_OK) return rc;
+    std::vector<double> an(L);
+    if ((rc = level_anorms(h, d_U, d_bc, s0, L, an.data(), st)) != PIT_OK) return rc;
+    const double bound = chain_bound(an.data(), L);
+    if (!(bound <= PIT_GATE))
+        return set_err(h, PIT_ECOND, "window [%d, %d): prod ||A_i||_inf = %.3e > %.0e (Section 7 gate)", s0, s0 + L, bound, PIT_GATE);
+    return product_window(h, s0, L, d_U, d_bc, d_R, d_carry, d_dU, (int*)d_info, st);
 }
 
 int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
@@ -460,10 +675,10 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     }
     unsigned long long tr[7] = {0, 0, 0, 0, 0, 0, 0};
     if (h->trace) CUDA_TRY(h, cudaMemcpy(tr, h->trace, sizeof(tr), cudaMemcpyDeviceToHost));
-    const long long v[15] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
+    const long long v[16] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
                              h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
-                             (long long)tr[4], (long long)tr[5], (long long)tr[6]};
-    for (int i = 0; i < n && i < 15; ++i) out[i] = v[i];
+                             (long long)tr[4], (long long)tr[5], (long long)tr[6], h->product_used ? 1 : 0};
+    for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
     return PIT_OK;
 }
 

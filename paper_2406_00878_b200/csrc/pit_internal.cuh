@@ -63,10 +63,11 @@ struct SolveParams {
     double newton_tol, lin_rtol, lin_atol;
     int newton_max, lin_max;
     long long* stats;            // [4] steps, inner iterations, depth, G
-    int mode;                    // 0 = Newton solve, 1 = single level solve (tests)
-    int level;                   // mode 1: level n (1-based)
-    const double* b_in;          // mode 1: right-hand side [ns]
-    double* x_out;               // mode 1: solution [ns]
+    int mode;                    // 0 = Newton solve, 1 = batch of independent level solves A_n x = b
+    int nb;                      // mode 1: number of right-hand sides (<= D)
+    int blev[MAXD];              // mode 1: level n (1-based) of right-hand side a; A_n taken at U level n
+    const double* bptr[MAXD];    // mode 1: right-hand sides [ns]
+    double* xptr[MAXD];          // mode 1: solutions [ns] (may alias bptr)
     int hmax;                    // on-chip engine: max rows of a CTA strip
     struct BarState* bs;         // on-chip engine: monotonic barrier state
     unsigned long long* trace;   // optional cycle accounting [7] (nullptr = off)

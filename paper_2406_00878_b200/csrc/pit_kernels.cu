@@ -126,6 +126,81 @@ __global__ void k_finish_norms(const double* __restrict__ part, int nparts, long
     if (threadIdx.x == 0) { norms[0] = sqrt(a[0] / (double)N); norms[1] = a[1]; }
 }
 
+
+// ----------------------------------------------------------------------------------------------------
+// (b2) building blocks of the literal Theorem 1 product form inside a Section 7 window.
+// ----------------------------------------------------------------------------------------------------
+struct MatvecJobs {
+    int n;
+    int lev[MAXD];                // A_lev (1-based level), taken at the iterate U
+    const double* x[MAXD];
+    double* y[MAXD];              // y = A_lev x   (may not alias x)
+};
+
+// y_j = A_{lev_j} x_j for a batch of vectors: the true (unscaled) diagonal block of Eq. (6) at U.
+__global__ void __launch_bounds__(BLOCK) k_matvec_batch(Prob P, const double* __restrict__ U, const double* __restrict__ ring,
+                                                        MatvecJobs J) {
+    const int j = blockIdx.y;
+    const int n = J.lev[j];
+    const double* Ul = U + (long long)(n - 1) * P.ns;
+    const double* ringn = ring ? ring + (long long)(n - 1) * P.ring_len : nullptr;
+    const double* x = J.x[j];
+    double* y = J.y[j];
+    for (long long p = (long long)blockIdx.x * BLOCK + threadIdx.x; p < P.ns; p += (long long)gridDim.x * BLOCK) {
+        const Nbr nb = neighbours(P, p);
+        const Vals v = stencil_values(P, Ul, ringn, p, nb);
+        const RJ o = residual_jacobian(P, v, nb, 0.0);
+        y[p] = o.aC * x[p] + o.aE * x[nb.e] + o.aW * x[nb.w] + o.aN * x[nb.n] + o.aS * x[nb.s];
+    }
+}
+
+// r~^m = sum_{j <= m} y^j over the window's levels, in place (the level scan of the RHS recursion,
+// r~^{n+1} = P^n r^{n+1} + r~^n).
+__global__ void k_level_prefix(long long ns, int L, double* __restrict__ Y) {
+    for (long long p = (long long)blockIdx.x * BLOCK + threadIdx.x; p < ns; p += (long long)gridDim.x * BLOCK) {
+        double acc = 0.0;
+        for (int m = 0; m < L; ++m) {
+            acc += Y[(long long)m * ns + p];
+            Y[(long long)m * ns + p] = acc;
+        }
+    }
+}
+
+// ||A_n||_inf (max absolute row sum) of levels n0..n0+L-1 at U: the Section 7 gate (R13 of
+// SURVEY: Gershgorin bound on the forward chain prod ||A_i||).  part[L][gridDim.x] partial maxima.
+__global__ void __launch_bounds__(BLOCK) k_anorm(Prob P, const double* __restrict__ U, const double* __restrict__ ring,
+                                                 int n0, double* __restrict__ part) {
+    __shared__ double red[NWARP * 1];
+    const int n = n0 + blockIdx.y;
+    const double* Ul = U + (long long)(n - 1) * P.ns;
+    const double* ringn = ring ? ring + (long long)(n - 1) * P.ring_len : nullptr;
+    double a[1] = {0.0};
+    for (long long p = (long long)blockIdx.x * BLOCK + threadIdx.x; p < P.ns; p += (long long)gridDim.x * BLOCK) {
+        const Nbr nb = neighbours(P, p);
+        const Vals v = stencil_values(P, Ul, ringn, p, nb);
+        const RJ o = residual_jacobian(P, v, nb, 0.0);
+        a[0] = fmax(a[0], fabs(o.aC) + fabs(o.aE) + fabs(o.aW) + fabs(o.aN) + fabs(o.aS));
+    }
+    block_reduce<0, 1>(a, red);
+    if (threadIdx.x == 0) part[(long long)blockIdx.y * gridDim.x + blockIdx.x] = a[0];
+}
+
+// U += dU over all levels, fused norm partials of dU (sum dU^2, max |dU|, nonfinite flag).
+__global__ void __launch_bounds__(BLOCK) k_update(long long N, double* __restrict__ U, const double* __restrict__ dU,
+                                                  double* __restrict__ part) {
+    __shared__ double red[NWARP * 3];
+    double a[3] = {0.0, 0.0, 0.0};
+    for (long long q = (long long)blockIdx.x * BLOCK + threadIdx.x; q < N; q += (long long)gridDim.x * BLOCK) {
+        const double d = dU[q];
+        U[q] += d;
+        a[0] += d * d;
+        a[1] = fmax(a[1], fabs(d));
+        if (!isfinite(d)) a[2] = 1.0;
+    }
+    block_reduce<1, 2>(a, red);
+    if (threadIdx.x == 0) { part[3 * blockIdx.x] = a[0]; part[3 * blockIdx.x + 1] = a[1]; part[3 * blockIdx.x + 2] = a[2]; }
+}
+
 // U_0: the caller's guess, or u^0 at every level.
 __global__ void k_init_iterate(long long ns, int nt, const double* u0, const double* guess,
                                double* U) {
@@ -173,19 +248,19 @@ __global__ void __launch_bounds__(BLOCK) k_newton(SolveParams S) {
         int ks[MAXD];
         int A = 0;
         for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ks[A++] = k;
-        if (S.mode == 1) { A = 1; ks[0] = 0; }
+        if (S.mode == 1) { A = S.nb; for (int a = 0; a < A; ++a) ks[a] = a; }
         // my pair = the one whose contiguous CTA block [a G / A, (a+1) G / A) contains g
         int me = 0;
         while (me + 1 < A && (long long)(me + 1) * G / A <= g) ++me;
         const int g0 = (int)((long long)me * G / A), g1 = (int)((long long)(me + 1) * G / A);
         const int kme = ks[me];
-        const int n = S.mode == 1 ? S.level : step - sS[kme] + 1;       // 1-based level
+        const int n = S.mode == 1 ? S.blev[me] : step - sS[kme] + 1;       // 1-based level
         const int slot = kme % S.D;
         const int buf = kme % S.B, nbuf = (kme + 1) % S.B;
         const Slot sl = slot_at(S.slotmem, ns, slot);
         const long long c = g - g0, C = g1 - g0;
         const long long p0 = c * ns / C, p1 = (c + 1) * ns / C;
-        const double* Ulev = S.mode == 1 ? S.U : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
+        const double* Ulev = S.mode == 1 ? S.U + (long long)(n - 1) * ns : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
         const double* uprev = n == 1 ? S.u0 : Ulev - ns;
         const double* ringn = S.ring ? S.ring + (long long)(n - 1) * P.ring_len : nullptr;
         double* partS = S.part + (long long)set * G * NPART;
@@ -200,7 +275,7 @@ __global__ void __launch_bounds__(BLOCK) k_newton(SolveParams S) {
                 const RJ o = residual_jacobian(P, v, nb, S.mode == 1 ? 0.0 : uprev[p]);
                 double rhs;
                 if (S.mode == 1) {
-                    rhs = S.b_in[p];
+                    rhs = S.bptr[me][p];
                 } else {
                     const double r = -o.G;                               // Newton rhs of Eq. (5)
                     a[1] += r * r;
@@ -350,7 +425,7 @@ __global__ void __launch_bounds__(BLOCK) k_newton(SolveParams S) {
                 if (pending) dx += alpha * sl.p[lp][p] + omega * sl.s[p];
                 sl.x[p] = dx;                        // du^n: the carry of level n+1 (same slot)
                 if (S.mode == 1) {
-                    S.x_out[p] = dx;
+                    S.xptr[me][p] = dx;
                 } else {
                     Unew[p] = Ulev[p] + dx;
                 }

@@ -218,12 +218,12 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
         int ks[MAXD];
         int A = 0;
         for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ks[A++] = k;
-        if (S.mode == 1) { A = 1; ks[0] = 0; }
+        if (S.mode == 1) { A = S.nb; for (int a = 0; a < A; ++a) ks[a] = a; }
         int me = 0;
         while (me + 1 < A && (long long)(me + 1) * G / A <= g) ++me;
         const int g0 = (int)((long long)me * G / A), g1 = (int)((long long)(me + 1) * G / A);
         const int kme = ks[me];
-        const int n = S.mode == 1 ? S.level : step - sS[kme] + 1;
+        const int n = S.mode == 1 ? S.blev[me] : step - sS[kme] + 1;
         const int slot = kme % S.D;
         const int buf = kme % S.B, nbuf = (kme + 1) % S.B;
         const Slot sl = slot_at(S.slotmem, ns, slot);
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
         const int c = g - g0, C = g1 - g0;
         const int r0 = (int)((long long)c * nyu / C), r1 = (int)((long long)(c + 1) * nyu / C);
         const int h = r1 - r0, npts = h * nxu;
-        const double* Ulev = S.mode == 1 ? S.U : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
+        const double* Ulev = S.mode == 1 ? S.U + (long long)(n - 1) * ns : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
         const double* uprev = n == 1 ? S.u0 : Ulev - ns;
         const double* ringn = S.ring ? S.ring + (long long)(n - 1) * P.ring_len : nullptr;
         double* Unew = S.mode == 1 ? nullptr : S.U + ((long long)nbuf * P.nt + (n - 1)) * ns;
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 bt[m] = 0.0; sr[m] = 0.0;
                 if (lrr[m] >= 0) {
                     if (S.mode == 1) {
-                        sr[m] = __ldcg(S.b_in + q);
+                        sr[m] = __ldcg(S.bptr[me] + q);
                     } else {
                         bt[m] = __ldcg(uprev + q);
                         sr[m] = n == 1 ? 0.0 : __ldcg(pX + q);
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                         const long long q = qbase + l;
                         double dx = x[m];
                         if (pending) dx += alpha * p_s[i] + omega * sr[m];
-                        if (S.mode == 1) S.x_out[q] = dx;
+                        if (S.mode == 1) S.xptr[me][q] = dx;
                         else {
                             pX[q] = dx;
                             Unew[q] = u_s[l + 2 * lr + W + 1] + dx;

@@ -94,7 +94,7 @@ def test_converged_solution_matches_oracle(name, engine):
     p = {"c1": lambda: W.config(1), "c2_small": lambda: W.config(2, n=24, nt=12), "c2": lambda: W.config(2),
          "paper_heat16": lambda: W.paper_heat(16), "paper_burgers12": lambda: W.paper_burgers(12),
          "ph": lambda: _rand_problems()[4], "dh_ragged": lambda: _rand_problems()[5]}[name]()
-    U, hist, nit, st, stats, seq = _parity(p, engine=engine)
+    U, hist, nit, st, stats, seq = _parity(p, engine=engine, inverse_mode=pit.PIT_INV_RECURRENCE)
     # the paper's accuracy tables are reproduced by the GPU path too
     if name == "paper_heat16":
         assert abs(np.abs(U - W.exact_field(p, p.exact)).max() / 1.15e-4 - 1) < 0.005
@@ -106,7 +106,7 @@ def test_converged_solution_matches_oracle(name, engine):
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_iteration_history_matches_oracle_allatonce(cfg, engine):
     p = W.config(1) if cfg == 1 else W.config(2, n=32, nt=16)
-    U, hist, nit, st, stats = gpu_solve(p, engine=engine)
+    U, hist, nit, st, stats = gpu_solve(p, engine=engine, inverse_mode=pit.PIT_INV_RECURRENCE)
     ref = O.solve_allatonce(p, tol=p.newton_tol)
     assert nit == ref.niter and st == ref.status
     for k in range(nit):
@@ -120,8 +120,8 @@ def test_iteration_history_matches_oracle_allatonce(cfg, engine):
 @pytest.mark.parametrize("depth", [1, 2, 3, 5, 8])
 def test_wavefront_depth_does_not_change_the_answer(depth, engine):
     p = W.config(2, n=20, nt=10)
-    U1, h1, n1, s1, st1 = gpu_solve(p, pipeline_depth=1, engine=1)
-    Ud, hd, nd, sd, std = gpu_solve(p, pipeline_depth=depth, engine=engine)
+    U1, h1, n1, s1, st1 = gpu_solve(p, pipeline_depth=1, engine=1, inverse_mode=pit.PIT_INV_RECURRENCE)
+    Ud, hd, nd, sd, std = gpu_solve(p, pipeline_depth=depth, engine=engine, inverse_mode=pit.PIT_INV_RECURRENCE)
     assert n1 == nd and s1 == sd
     assert normwise_rel(Ud, U1) <= 1e-13
     assert std["depth"] == min(depth, 30)
@@ -130,10 +130,10 @@ def test_wavefront_depth_does_not_change_the_answer(depth, engine):
 @pytest.mark.parametrize("engine", [1, 2])
 def test_deterministic_and_host_path_identical(engine):
     p = W.config(2, n=24, nt=8)
-    U1, h1, n1, s1, _ = gpu_solve(p, engine=engine)
-    U2, h2, n2, s2, _ = gpu_solve(p, engine=engine)
+    U1, h1, n1, s1, _ = gpu_solve(p, engine=engine, inverse_mode=pit.PIT_INV_RECURRENCE)
+    U2, h2, n2, s2, _ = gpu_solve(p, engine=engine, inverse_mode=pit.PIT_INV_RECURRENCE)
     assert np.array_equal(U1, U2) and np.array_equal(h1, h2)
-    Uh, hh, nh, sh = pit.solve(p, engine=engine)
+    Uh, hh, nh, sh = pit.solve(p, engine=engine, inverse_mode=pit.PIT_INV_RECURRENCE)
     assert np.array_equal(Uh, U1) and nh == n1 and sh == s1
 
 
