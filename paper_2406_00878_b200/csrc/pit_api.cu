@@ -307,6 +307,14 @@ static int grid_for(long long n, int sms) {
     return (int)std::max<long long>(1, std::min<long long>(g, (long long)sms * 8));
 }
 
+static void launch_resjac(pit_handle* h, int grid, cudaStream_t st, const double* U, const double* u0, const double* ring,
+                          double* R, double* diag, double* part) {
+    if (h->P.pde == PIT_BURGERS && h->P.m2 == 0.0)
+        k_resjac<1><<<grid, BLOCK, 0, st>>>(h->P, U, u0, ring, R, diag, part);
+    else
+        k_resjac<0><<<grid, BLOCK, 0, st>>>(h->P, U, u0, ring, R, diag, part);
+}
+
 static SolveParams base_params(pit_handle* h) {
     SolveParams S;
     std::memset(&S, 0, sizeof(S));
@@ -388,7 +396,7 @@ static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, 
     double prevmax = INFINITY;
     const int gr = std::min(grid_for(N, h->sms), 1024);
     for (int k = 0; k < kmax; ++k) {
-        k_resjac<<<gr, BLOCK, 0, st>>>(P, U, d_u0, ring, h->pf_R, nullptr, h->d_small);
+        launch_resjac(h, gr, st, U, d_u0, ring, h->pf_R, nullptr, h->d_small);
         CUDA_TRY(h, cudaGetLastError());
         k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, gr, N, h->d_small + 2048);
         CUDA_TRY(h, cudaGetLastError());
@@ -512,7 +520,7 @@ int pit_residual_device(pit_handle* h, const double* d_U, const double* d_u0, co
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const long long N = h->P.ns * h->P.nt;
     const int grid = std::min(grid_for(N, h->sms), 1024);
-    k_resjac<<<grid, BLOCK, 0, st>>>(h->P, d_U, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_R, d_diag, h->d_small);
+    launch_resjac(h, grid, st, d_U, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_R, d_diag, h->d_small);
     CUDA_TRY(h, cudaGetLastError());
     if (d_norms) {
         k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, grid, N, d_norms);

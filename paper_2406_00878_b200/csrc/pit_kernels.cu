@@ -90,26 +90,70 @@ __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 // (a) all-level residual + diagonal, fused partial norms.  One thread per unknown (grid-stride over
 // the [nt][ns] space-time array); the stencil neighbours and u^{n-1} are L1/L2 hits.
 // ----------------------------------------------------------------------------------------------------
+// Residual and diagonal coefficient only (kernel a).  LAW 1 = Burgers with constant viscosity (m2 = 0):
+// G = u_C - u_prev + tau[(u_E^2 - u_W^2)/(4h_x) + (u_N^2 - u_S^2)/(4h_y) - m0 (Laplacian)], a_C constant.
+template <int LAW>
+__device__ __forceinline__ void res_diag(const Prob& P, const Vals& v, double uprev, double& G, double& aC) {
+    if (LAW == 1) {
+        const double conv = 0.5 * ((v.e * v.e - v.w * v.w) * P.i2hx + (v.n * v.n - v.s * v.s) * P.i2hy);
+        const double lap = (v.e + v.w - 2.0 * v.c) * P.ihx2 + (v.n + v.s - 2.0 * v.c) * P.ihy2;
+        G = (v.c - uprev) + P.dt * (conv - P.m0 * lap);
+        aC = 1.0 + 2.0 * P.dt * P.m0 * (P.ihx2 + P.ihy2);
+        return;
+    }
+    const RJ o = residual_jacobian_raw(P, v, uprev);
+    G = o.G;
+    aC = o.aC;
+}
+
+template <int LAW>
 __global__ void __launch_bounds__(BLOCK) k_resjac(Prob P, const double* __restrict__ U, const double* __restrict__ u0,
                                                   const double* __restrict__ ring, double* __restrict__ R,
                                                   double* __restrict__ diag, double* __restrict__ part) {
+    constexpr int RB = 4;                      // rows per iteration: all their loads are issued before any use
     __shared__ double red[NWARP * 2];
-    const long long N = P.ns * P.nt;
+    const int nxu = P.nxu, nyu = P.nyu;
+    const int nxp = P.nx + 1;
+    const int rows = P.nt * nyu;
+    const int groups = (rows + RB - 1) / RB;
     double a[2] = {0.0, 0.0};
-    for (long long q = (long long)blockIdx.x * BLOCK + threadIdx.x; q < N; q += (long long)gridDim.x * BLOCK) {
-        const int n = (int)(q / P.ns);                 // 0-based level
-        const long long p = q - (long long)n * P.ns;
-        const double* Ul = U + (long long)n * P.ns;
-        const double* ringn = ring ? ring + (long long)n * P.ring_len : nullptr;
-        const double uprev = n == 0 ? u0[p] : Ul[p - P.ns];
-        const Nbr nb = neighbours(P, p);
-        const Vals v = stencil_values(P, Ul, ringn, p, nb);
-        const RJ o = residual_jacobian(P, v, nb, uprev);
-        const double r = -o.G;
-        R[q] = r;
-        if (diag) diag[q] = o.aC;
-        a[0] += r * r;
-        a[1] = fmax(a[1], fabs(r));
+    for (int grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+        for (int i = threadIdx.x; i < nxu; i += BLOCK) {
+            const bool he = P.bc == 1 || i + 1 < nxu, hw = P.bc == 1 || i > 0;
+            const int ie = i + 1 < nxu ? i + 1 : 0, iw = i > 0 ? i - 1 : nxu - 1;
+            Vals v[RB];
+            double up[RB];
+            long long q[RB];
+            #pragma unroll
+            for (int t = 0; t < RB; ++t) {
+                const int row = min(grp * RB + t, rows - 1);
+                const int n = row / nyu, j = row - n * nyu;             // level n (0-based), row j
+                const double* Ul = U + (long long)n * P.ns;
+                const double* Up = n == 0 ? u0 : Ul - P.ns;
+                const double* ringn = ring ? ring + (long long)n * P.ring_len : nullptr;
+                const long long rb = (long long)j * nxu;
+                const bool hn = P.bc == 1 || j + 1 < nyu, hs = P.bc == 1 || j > 0;
+                const long long rn = j + 1 < nyu ? rb + nxu : 0, rs = j > 0 ? rb - nxu : (long long)(nyu - 1) * nxu;
+                v[t].c = __ldg(Ul + rb + i);
+                v[t].e = he ? __ldg(Ul + rb + ie) : (ringn ? __ldg(ringn + 2 * nxp + (P.ny - 1) + j) : 0.0);
+                v[t].w = hw ? __ldg(Ul + rb + iw) : (ringn ? __ldg(ringn + 2 * nxp + j) : 0.0);
+                v[t].n = hn ? __ldg(Ul + rn + i) : (ringn ? __ldg(ringn + nxp + i + 1) : 0.0);
+                v[t].s = hs ? __ldg(Ul + rs + i) : (ringn ? __ldg(ringn + i + 1) : 0.0);
+                up[t] = __ldg(Up + rb + i);
+                q[t] = (long long)n * P.ns + rb + i;
+            }
+            #pragma unroll
+            for (int t = 0; t < RB; ++t) {
+                if (grp * RB + t >= rows) continue;
+                double G, aC;
+                res_diag<LAW>(P, v[t], up[t], G, aC);
+                const double r = -G;
+                __stcs(R + q[t], r);                                   // streaming stores: R, diag not re-read here
+                if (diag) __stcs(diag + q[t], aC);
+                a[0] += r * r;
+                a[1] = fmax(a[1], fabs(r));
+            }
+        }
     }
     block_reduce<1, 1>(a, red);
     if (threadIdx.x == 0) {
