@@ -75,16 +75,17 @@ typedef struct {
     double  newton_tol;    /* stop on max|dU_k| <= newton_tol (> 0; BASELINE: 1e-12) */
     int32_t newton_max;    /* max Newton iterations (1..256) */
     double  lin_rtol;      /* per-level solve: ||b~ - A~ x||_2 <= lin_rtol ||b~||_2 (A~ = diag-scaled A_n);
-                              0 = default 1e-13 */
-    double  lin_atol;      /* absolute floor on that residual; 0 = default 1e-4 * newton_tol */
+                              0 = default 1e-10 */
+    double  lin_atol;      /* ... or RMS(b~ - A~ x) = ||.||_2 / sqrt(ns) <= lin_atol; 0 = default 1e-4 * newton_tol */
     int32_t lin_max;       /* per-level BiCGSTAB iteration cap; 0 = default 1000 */
     int32_t inverse_mode;  /* PIT_INV_*; AUTO = recurrence unless the product window admits all levels */
     int32_t window;        /* product-form window length; 0 = auto from the Section 7 gate */
     int32_t pipeline_depth;/* Newton iterations in flight in the level wavefront; 0 = auto */
     int32_t device;        /* CUDA device ordinal */
-    int32_t engine;        /* 0 = auto (on-chip if the level strips fit registers + shared memory),
-                              1 = global-state engine (any size), 2 = on-chip engine (PIT_EINVAL if it
-                              does not fit) */
+    int32_t engine;        /* 0 = auto (column-blocked on-chip if it fits, else strip on-chip, else global),
+                              1 = global-state engine (any size), 2 = strip on-chip engine, 3 = column-blocked
+                              on-chip engine (nx = 256 or 512 unknowns per row); 2/3: PIT_EINVAL if they do
+                              not fit the registers + shared memory of one SM per CTA */
 } pit_config;
 
 typedef struct pit_handle pit_handle;
@@ -149,11 +150,12 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * out[2] = pipeline depth used, out[3] = grid CTAs, out[4] = kernel launches of the last solve,
  * out[5] = device time of the persistent Newton kernel of the last solve [ns] (CUDA events on the
  * launching stream), out[6] = device time of the iterate-initialisation kernel [ns], out[7] = engine
- * (1 global-state, 2 on-chip), out[8..14] = on-chip engine cycle accounting summed over CTAs
+ * (1 global-state, 2 strip on-chip, 3 column-blocked on-chip), out[8..14] = on-chip engine cycle accounting summed over CTAs
  * (prologue, phase 1, phase 2, epilogue, grid barriers, scalar reductions, step bookkeeping) when the
  * environment variable PIT_TRACE was set at pit_create (zeros otherwise), out[15] = 1 if the last solve
  * inverted Eq. (6) with the (b2) product form (inverse_mode PRODUCT_WINDOW, or AUTO with the whole horizon
- * inside the Section 7 gate), 0 for the on-device level recurrence. */
+ * inside the Section 7 gate), 0 for the on-device level recurrence, out[16] = BiCGSTAB iterations summed
+ * over all (level, iteration) pairs (on-chip engine), out[17 + k] = those of Newton iteration k. */
 int pit_stats(pit_handle* h, int64_t* out, int32_t n);
 
 const char* pit_strerror(int code);

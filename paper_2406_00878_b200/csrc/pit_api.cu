@@ -41,7 +41,7 @@ struct pit_handle {
     GridBar* bar = nullptr;
     double* hist = nullptr;       // [newton_max][4]
     int* info = nullptr;          // [2]
-    long long* stats = nullptr;   // [4]
+    long long* stats = nullptr;   // [8 + MAXK]: steps, max-per-step inner its, D, G, sum over pairs, -, -, -, per-k sums
     double* d_u0 = nullptr;       // host-path staging
     double* d_bc = nullptr;
     double* d_small = nullptr;    // [2 * 1024] scratch for kernel (a) partials + norms
@@ -153,6 +153,16 @@ static const void* onchip_fn_t(int ppt) {
     }
 }
 
+template <bool TR, int LAW>
+static const void* col_fn_t(int rmax) {
+    return rmax <= 4 ? (const void*)k_newton_col<4, TR, LAW> : (const void*)k_newton_col<8, TR, LAW>;
+}
+
+static const void* col_fn(int rmax, bool trace, int law) {
+    if (law == 1) return trace ? col_fn_t<true, 1>(rmax) : col_fn_t<false, 1>(rmax);
+    return trace ? col_fn_t<true, 0>(rmax) : col_fn_t<false, 0>(rmax);
+}
+
 // LAW 1 = viscous Burgers with constant viscosity (m2 = 0): specialised matvec coefficients.
 static const void* onchip_fn(int ppt, bool trace, int law) {
     if (law == 1) return trace ? onchip_fn_t<true, 1>(ppt) : onchip_fn_t<false, 1>(ppt);
@@ -169,7 +179,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     if (!h) return PIT_ENOMEM;
     h->cfg = *cfg;
     pit_config& c = h->cfg;
-    if (c.lin_rtol == 0.0) c.lin_rtol = 1e-13;
+    if (c.lin_rtol == 0.0) c.lin_rtol = 1e-10;
     if (c.lin_atol == 0.0) c.lin_atol = 1e-4 * c.newton_tol;
     if (c.lin_max == 0) c.lin_max = 1000;
 
@@ -211,7 +221,33 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     // thread, <= 200 KB shared).  Otherwise the global-state engine (any size).
     const int Dmax = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : 8, c.newton_max));
     const int law = (c.pde == PIT_BURGERS && c.m2 == 0.0) ? 1 : 0;
-    if (c.engine != 1 && P.nxu <= BLOCK2 && h->sms <= 160) {
+    h->law = law;
+    // Column-blocked on-chip engine (engine 3): nx = 256 or 512, one 512-thread CTA per SM, a thread owns a
+    // column of at most RMAX (4 or 8) strip rows.  Preferred whenever it fits.
+    if ((c.engine == 0 || c.engine == 3) && (P.nxu == 256 || P.nxu == 512) && h->sms <= 160) {
+        const int Gr = BLOCK3 / P.nxu;
+        for (int D = Dmax; D >= 1 && h->engine != 3; --D) {
+            const int C = h->sms / D;
+            if (C < 1) continue;
+            const int hmax = (P.nyu + C - 1) / C;
+            const int rows = (hmax + Gr - 1) / Gr;
+            const int rmax = rows <= 4 ? 4 : (rows <= 8 ? 8 : 0);
+            if (!rmax) continue;
+            const size_t smem = (size_t)((2 * hmax + 2) * (P.nxu + 2) + (law == 1 ? 4 : 5) * rmax * BLOCK3) * sizeof(double);
+            if (smem > 220 * 1024) continue;
+            bool ok = true;
+            int occ3 = 0;
+            for (bool tr : {false, true}) {
+                const void* fn = col_fn(rmax, tr, law);
+                ok = ok && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, fn, BLOCK3, smem) == cudaSuccess && occ3 >= 1;
+            }
+            if (!ok) { cudaGetLastError(); continue; }
+            h->engine = 3; h->D = D; h->ppt = rmax; h->hmax = hmax; h->smem2 = smem; h->G = h->sms; h->occ = 1;
+        }
+        if (h->engine != 3 && c.engine == 3) { delete h; return PIT_EINVAL; }
+    }
+    if ((c.engine == 0 || c.engine == 2) && h->engine == 1 && P.nxu <= BLOCK2 && h->sms <= 160) {
         for (int D = Dmax; D >= 1 && h->engine != 2; --D) {
             const int C = h->sms / D;
             if (C < 1) continue;
@@ -235,11 +271,10 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
                 continue;
             }
             h->engine = 2; h->D = D; h->ppt = ppt; h->hmax = hmax; h->smem2 = smem; h->G = h->sms; h->occ = 1;
-            h->law = law;
         }
         if (h->engine != 2 && c.engine == 2) { delete h; return PIT_EINVAL; }
     }
-    if (h->engine != 2) {
+    if (h->engine == 1) {
         int occ = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_newton, BLOCK, 0) != cudaSuccess || occ < 1) {
             cudaGetLastError();
@@ -265,12 +300,12 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         (rc = dalloc(h, &h->bar, 1)) ||
         (rc = dalloc(h, &h->hist, (size_t)(4 * c.newton_max))) ||
         (rc = dalloc(h, &h->info, 2)) ||
-        (rc = dalloc(h, &h->stats, 4)) ||
+        (rc = dalloc(h, &h->stats, 8 + MAXK)) ||
         (rc = dalloc(h, &h->d_u0, (size_t)P.ns)) ||
         (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
         (rc = dalloc(h, &h->d_small, 2 * 1024 + 2)) ||
         (rc = dalloc(h, &h->bs, 1)) ||
-        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 7)))) {
+        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 11)))) {
         free_all(h);
         delete h;
         return rc;
@@ -278,7 +313,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     bool ev_ok = true;
     for (auto& e : h->ev) ev_ok = ev_ok && cudaEventCreate(&e) == cudaSuccess;
     if (!ev_ok || cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess ||
-        cudaMemset(h->stats, 0, 4 * sizeof(long long)) != cudaSuccess) {
+        cudaMemset(h->stats, 0, (8 + MAXK) * sizeof(long long)) != cudaSuccess) {
         cudaGetLastError();
         free_all(h);
         delete h;
@@ -339,15 +374,20 @@ static SolveParams base_params(pit_handle* h) {
 static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
     void* args[] = {(void*)&S};
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
-    if (h->engine == 2) {
+    if (h->engine >= 2) {
         S.hmax = h->hmax;
         S.bs = h->bs;
         S.trace = h->trace;
         S.x0carry = getenv("PIT_X0") ? atoi(getenv("PIT_X0")) : 1;   // default: start from du^{n-1}
-        if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 7 * sizeof(unsigned long long), st));
+        if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 11 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
-        CUDA_TRY(h, cudaLaunchCooperativeKernel(onchip_fn(h->ppt, h->trace != nullptr, h->law), dim3(h->G), dim3(BLOCK2), args,
-                                                h->smem2, st));
+        CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
+        if (h->engine == 3)
+            CUDA_TRY(h, cudaLaunchCooperativeKernel(col_fn(h->ppt, h->trace != nullptr, h->law), dim3(h->G), dim3(BLOCK3), args,
+                                                    h->smem2, st));
+        else
+            CUDA_TRY(h, cudaLaunchCooperativeKernel(onchip_fn(h->ppt, h->trace != nullptr, h->law), dim3(h->G), dim3(BLOCK2),
+                                                    args, h->smem2, st));
     } else {
         CUDA_TRY(h, cudaMemsetAsync(h->bar, 0, sizeof(GridBar), st));
         CUDA_TRY(h, cudaLaunchCooperativeKernel((void*)k_newton, dim3(h->G), dim3(BLOCK), args, 0, st));
@@ -672,7 +712,7 @@ int pit_product_window_device(pit_handle* h, int32_t s0, int32_t L, const double
 
 int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     if (!h || !out || n < 1) return PIT_EINVAL;
-    long long s[4] = {0, 0, 0, 0};
+    long long s[8 + MAXK];
     CUDA_TRY(h, cudaSetDevice(h->device));
     CUDA_TRY(h, cudaMemcpy(s, h->stats, sizeof(s), cudaMemcpyDeviceToHost));
     float t_init = 0.f, t_newton = 0.f;
@@ -681,12 +721,14 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
         CUDA_TRY(h, cudaEventElapsedTime(&t_init, h->ev[0], h->ev[1]));
         CUDA_TRY(h, cudaEventElapsedTime(&t_newton, h->ev[2], h->ev[3]));
     }
-    unsigned long long tr[7] = {0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tr[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (h->trace) CUDA_TRY(h, cudaMemcpy(tr, h->trace, sizeof(tr), cudaMemcpyDeviceToHost));
-    const long long v[16] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
+    const long long v[17] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
                              h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
-                             (long long)tr[4], (long long)tr[5], (long long)tr[6], h->product_used ? 1 : 0};
-    for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
+                             (long long)tr[4], (long long)tr[5], (long long)tr[6], h->product_used ? 1 : 0, s[4]};
+    for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];
+    for (int i = 17; i < n && i < 17 + MAXK; ++i) out[i] = s[8 + (i - 17)];
+    for (int i = 17 + MAXK; i < n && i < 17 + MAXK + 4; ++i) out[i] = (long long)tr[7 + (i - 17 - MAXK)];
     return PIT_OK;
 }
 

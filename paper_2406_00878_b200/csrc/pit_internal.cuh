@@ -210,12 +210,16 @@ __device__ __forceinline__ void block_reduce(double (&a)[NS + NM], double* sm /*
         #pragma unroll
         for (int i = 0; i < N; ++i) sm[w * N + i] = a[i];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (w == 0) {
         #pragma unroll
         for (int i = 0; i < N; ++i) {
-            double s = sm[i];
-            for (int k = 1; k < NWARP; ++k) s = i < NS ? s + sm[k * N + i] : fmax(s, sm[k * N + i]);
-            a[i] = s;
+            double v = l < NWARP ? sm[l * N + i] : 0.0;
+            #pragma unroll
+            for (int o = NWARP / 2; o > 0; o >>= 1) {
+                const double y = __shfl_xor_sync(0xffffffffu, v, o);
+                v = i < NS ? v + y : fmax(v, y);
+            }
+            a[i] = v;
         }
     }
     __syncthreads();

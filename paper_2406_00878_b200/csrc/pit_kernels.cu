@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(BLOCK) k_newton(SolveParams S) {
     int klo = 0;
     int last_done = -1;                        // last completed Newton iteration
     long long total_inner = 0;
-    const double rtol2 = S.lin_rtol * S.lin_rtol, atol2 = S.lin_atol * S.lin_atol;
+    const double rtol2 = S.lin_rtol * S.lin_rtol;
+    const double atol2 = S.lin_atol * S.lin_atol * (double)P.ns;     // lin_atol bounds the RMS residual
 
     for (int step = 1;; ++step) {
         // ---- active (level, iteration) pairs of this wavefront step, iteration ascending ----
@@ -560,3 +561,4 @@ __global__ void __launch_bounds__(BLOCK) k_newton(SolveParams S) {
 }  // namespace pit
 
 #include "pit_newton_onchip.cuh"
+#include "pit_newton_col.cuh"

@@ -1,0 +1,527 @@
+// pit_newton_col.cuh — the COLUMN-BLOCKED on-chip engine (included by pit_kernels.cu after the strip engine).
+//
+// Same method, schedule, barriers, reductions and stop rule as k_newton_onchip; only the point layout of a
+// strip changes.  A thread owns one grid COLUMN of (a sub-strip of) its CTA's rows, so
+//   * the N/S neighbours of every matvec come from the thread's own registers (the register-blocked
+//     5-point stencil), only E/W neighbours go through shared memory (2 loads + 1 store per point);
+//   * u^n of the strip (one halo row each side) is staged once per step in shared memory and the
+//     coefficients are recomputed from it (registers are kept for the Krylov vectors: 128 per thread);
+//   * r/s and p are registers; x, r^0 (= b~ - A~ x0), v, t (and 1/a_C for the general law) are shared.
+// Applies when nx (unknowns per row) is 256 or 512: 512 threads = 1 or 2 column groups; a column group
+// splits the strip rows in two sub-strips whose boundary rows are exchanged through the shared operand.
+#pragma once
+
+namespace pit {
+
+constexpr int BLOCK3 = 512;
+
+template <int RMAX, bool TRACE, int LAW>
+__global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
+    extern __shared__ double smem[];
+    const Prob P = S.P;
+    const long long ns = P.ns;
+    const int nxu = P.nxu, nyu = P.nyu;
+    const int G = S.G, g = blockIdx.x, tid = threadIdx.x;
+    const int W = nxu + 2;
+    const int HM = S.hmax;
+    double* const u_s = smem;                          // [HM+2][W] u of the strip rows + halo rows (+ ring / wrap columns)
+    double* const op_s = u_s + (HM + 2) * W;           // [HM][W] matvec operand (E/W exchange)
+    double* const v_s = op_s + HM * W;                 // [RMAX][BLOCK3]
+    double* const t_s = v_s + RMAX * BLOCK3;           // [RMAX][BLOCK3]
+    double* const x_s = t_s + RMAX * BLOCK3;           // [RMAX][BLOCK3] BiCGSTAB iterate (-> du^n)
+    double* const bt_s = x_s + RMAX * BLOCK3;          // [RMAX][BLOCK3] shadow residual r^0 (and b~)
+    double* const ci_s = bt_s + RMAX * BLOCK3;         // [RMAX][BLOCK3] 1/a_C (LAW 0 only)
+    __shared__ int sS[MAXK];
+    __shared__ double red[NWARP2 * NPART];
+    __shared__ double s_hp_big[4 * GMAX2];
+    __shared__ double s_red[5 * GMAX2 + 8];
+    __shared__ double hacc[MAXD][4];
+    __shared__ double prevmax_s;
+    if (tid == 0) {
+        const int D = S.D;
+        for (int k = 0; k < S.newton_max; ++k) {
+            int st = k == 0 ? 1 : sS[k - 1] + 1;
+            if (k >= D && sS[k - D] + P.nt > st) st = sS[k - D] + P.nt;
+            sS[k] = st;
+        }
+        prevmax_s = INFINITY;
+    }
+    if (tid < MAXD * 4) hacc[tid / 4][tid % 4] = 0.0;
+    __syncthreads();
+
+    unsigned ep = 0;
+    unsigned hi[2] = {0u, 0u};
+    long long prof[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long t_last = clock64();
+    auto flush_prof = [&]() {
+        if (TRACE && tid == 0)
+            for (int j = 0; j < 11; ++j) atomicAdd(S.trace + j, (unsigned long long)prof[j]);
+    };
+    const int newton_max = S.mode == 0 ? S.newton_max : 1;
+    int set = 0, klo = 0, last_done = -1;
+    long long total_inner = 0;
+    const double rtol2 = S.lin_rtol * S.lin_rtol;
+    const double atol2 = S.lin_atol * S.lin_atol * (double)P.ns;     // lin_atol bounds the RMS residual
+    const int Gr = BLOCK3 / nxu;                       // column groups (1 or 2)
+    const int col = tid % nxu, grp = tid / nxu;
+    const double ci_const = 1.0 / (1.0 + 2.0 * P.dt * P.m0 * (P.ihx2 + P.ihy2));   // LAW 1: a_C is constant
+
+    for (int step = 1;; ++step) {
+        while (klo < newton_max && step > sS[klo] + P.nt - 1) ++klo;
+        int ks[MAXD];
+        int A = 0;
+        for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ks[A++] = k;
+        if (S.mode == 1) { A = S.nb; for (int a = 0; a < A; ++a) ks[a] = a; }
+        int me = 0;
+        while (me + 1 < A && (long long)(me + 1) * G / A <= g) ++me;
+        const int g0 = (int)((long long)me * G / A), g1 = (int)((long long)(me + 1) * G / A);
+        const int kme = ks[me];
+        const int n = S.mode == 1 ? S.blev[me] : step - sS[kme] + 1;
+        const int slot = kme % S.D;
+        const int buf = kme % S.B, nbuf = (kme + 1) % S.B;
+        const Slot sl = slot_at(S.slotmem, ns, slot);
+        double* const pBT = sl.bt;  double* const pX = sl.x;
+        double* const pS = sl.s;    double* const pT = sl.t;  double* const pP = sl.p[0];  double* const pV = sl.v[0];
+        double* const pR = sl.r;    double* const pV2 = sl.v[1];
+        const int c = g - g0, C = g1 - g0;
+        const int r0 = (int)((long long)c * nyu / C), r1 = (int)((long long)(c + 1) * nyu / C);
+        const int h = r1 - r0;
+        const double* Ulev = S.mode == 1 ? S.U + (long long)(n - 1) * ns : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
+        const double* uprev = n == 1 ? S.u0 : Ulev - ns;
+        const double* ringn = S.ring ? S.ring + (long long)(n - 1) * P.ring_len : nullptr;
+        double* Unew = S.mode == 1 ? nullptr : S.U + ((long long)nbuf * P.nt + (n - 1)) * ns;
+        double* hp = S.hpart + (long long)(step & 1) * G * 4;
+        // this thread's sub-strip of rows [R0, R1) (strip-local), column col
+        const int R0 = (int)((long long)grp * h / Gr), R1 = (int)((long long)(grp + 1) * h / Gr);
+        const int hs = R1 - R0;
+        const bool own_top = R0 == 0, own_bot = R1 == h;          // sub-strip touches the CTA's halo rows
+        const bool top_valid = P.bc == 1 || r0 > 0, bot_valid = P.bc == 1 || r1 < nyu;
+        const int top_row = r0 == 0 ? nyu - 1 : r0 - 1, bot_row = r1 == nyu ? 0 : r1;
+        const long long qc = (long long)(r0 + R0) * nxu + col;      // global index of the sub-strip's first point
+        auto q_of = [&](int r) { return qc + (long long)r * nxu; };
+        auto sidx = [&](int r) { return (R0 + r) * W + col + 1; };   // op_s index of own point r
+        auto uidx = [&](int r) { return (R0 + r + 1) * W + col + 1; };   // u_s index of own point r
+
+        double sr[RMAX], pp[RMAX];
+        auto X = [&](int r) -> double& { return x_s[r * BLOCK3 + tid]; };
+        auto BT = [&](int r) -> double& { return bt_s[r * BLOCK3 + tid]; };
+
+        // ---- prologue -----------------------------------------------------------------------------
+        const bool x0c = S.x0carry && S.mode == 0 && n > 1;
+        double xhS = 0.0, xhN = 0.0;          // carry across the CTA boundary rows (x0 operand)
+        double up[RMAX];
+        // stage u of the own column, rows -1 .. hs (the sub-strip plus one row each side), with the E/W halo
+        // columns (periodic wrap copy or Dirichlet ring) written by the edge columns
+        // (cp.async for values inside the domain, so all of a thread's row loads are in flight at once)
+        auto stage_u = [&](int ui, int gr, int gc) {
+            bool inside = true;
+            if (P.bc == 1) {
+                gr = gr < 0 ? gr + nyu : (gr >= nyu ? gr - nyu : gr);
+                gc = gc < 0 ? gc + nxu : (gc >= nxu ? gc - nxu : gc);
+            } else {
+                inside = gr >= 0 && gr < nyu && gc >= 0 && gc < nxu;
+            }
+            if (inside) {
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(u_s + ui);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(Ulev + (long long)gr * nxu + gc)
+                             : "memory");
+            } else {
+                u_s[ui] = node_ext(P, Ulev, ringn, gr, gc);
+            }
+        };
+        #pragma unroll 1
+        for (int r = -1; r <= hs; ++r) {
+            if (hs == 0) break;
+            const int ui = uidx(r), gr = r0 + R0 + r;
+            stage_u(ui, gr, col);
+            if (col == 0) stage_u(ui - 1, gr, -1);              // W halo column: wrap or ring
+            if (col == nxu - 1) stage_u(ui + 1, gr, nxu);       // E halo column
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        #pragma unroll
+        for (int r = 0; r < RMAX; ++r) {
+            up[r] = 0.0; sr[r] = 0.0;
+            if (r < hs) {
+                if (S.mode == 1) {
+                    sr[r] = __ldcg(S.bptr[me] + q_of(r));
+                } else {
+                    up[r] = __ldcg(uprev + q_of(r));
+                    sr[r] = n == 1 ? 0.0 : __ldcg(pX + q_of(r));
+                }
+                if (P.bc != 1) {
+                    if (col == 0) op_s[sidx(r) - 1] = 0.0;
+                    if (col == nxu - 1) op_s[sidx(r) + 1] = 0.0;
+                }
+            }
+        }
+        if (x0c && hs > 0) {
+            if (own_top && top_valid) xhS = __ldcg(pX + (long long)top_row * nxu + col);
+            if (own_bot && bot_valid) xhN = __ldcg(pX + (long long)bot_row * nxu + col);
+        }
+        PMARK(7);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        PMARK(8);
+        // operand accessors: N/S from registers inside the sub-strip, shared memory across the column-group
+        // boundary, the halo register across the CTA boundary; E/W from shared memory
+        auto opN = [&](const double (&o)[RMAX], int r, double haloN) -> double {
+            if (r + 1 < hs) return o[r + 1];
+            return own_bot ? haloN : op_s[sidx(r) + W];
+        };
+        auto opS = [&](const double (&o)[RMAX], int r, double haloS) -> double {
+            if (r > 0) return o[r - 1];
+            return own_top ? haloS : op_s[sidx(r) - W];
+        };
+        auto put_op = [&](int r, double val) {
+            const int si = sidx(r);
+            op_s[si] = val;
+            if (P.bc == 1) {
+                if (col == 0) op_s[si + nxu] = val;
+                if (col == nxu - 1) op_s[si - nxu] = val;
+            }
+        };
+        auto coef = [&](int r) -> Off {
+            const int ui = uidx(r);
+            const Vals uv = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], u_s[ui - W]};
+            return offdiag_law<LAW>(P, uv);
+        };
+        auto cinv = [&](int r) -> double { return LAW == 1 ? ci_const : ci_s[r * BLOCK3 + tid]; };
+        {
+            double a[4] = {0.0, 0.0, 0.0, 0.0};  // sum r0^2, sum r^2, sum b~^2 | max |r|
+            #pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+                pp[r] = 0.0;
+                if (r >= hs) continue;
+                const int ui = uidx(r);
+                const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], u_s[ui - W]};
+                const RJ o = residual_jacobian_raw(P, v, up[r]);
+                double rhs;
+                if (S.mode == 1) {
+                    rhs = sr[r];
+                } else {
+                    const double res = -o.G;
+                    a[1] += res * res;
+                    a[3] = fmax(a[3], fabs(res));
+                    rhs = res + sr[r];                 // r^n + du^{n-1}  (row n of Eq. 7)
+                }
+                const double ci = 1.0 / o.aC;
+                if (LAW != 1) ci_s[r * BLOCK3 + tid] = ci;
+                const double x0 = x0c ? sr[r] : 0.0;
+                X(r) = x0;
+                sr[r] = rhs * ci;                      // b~ (r0 once the x0 matvec is subtracted)
+                a[2] += sr[r] * sr[r];
+                if (x0c) { pp[r] = x0; put_op(r, x0); }
+            }
+            PMARK(9);
+            if (x0c) {
+                __syncthreads();
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= hs) continue;
+                    const int si = sidx(r);
+                    const Off o = coef(r);
+                    sr[r] -= pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, xhN) +
+                                                o.s * opS(pp, r, xhS));
+                }
+            }
+            #pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+                if (r >= hs) continue;
+                BT(r) = sr[r];                         // r0, and the BiCGSTAB shadow vector r^0 = r0
+                a[0] += sr[r] * sr[r];
+                const int R = R0 + r;
+                if (R == 0 || R == h - 1) pBT[q_of(r)] = sr[r];
+            }
+            PMARK(10);
+            block_reduce2<3, 1>(a, red);
+            if (tid == 0) {
+                S.part[((long long)set * G + g) * NPART] = a[0];
+                S.part[((long long)set * G + g) * NPART + 1] = a[2];
+                hp[g * 4 + 0] = a[1];
+                hp[g * 4 + 1] = a[3];
+            }
+        }
+        PMARK(0);
+        bar_sync(S.bs, G, ep, false, hi);
+        PMARK(4);
+        double bnorm2, rho;
+        {
+            double o[2];
+            pair_reduce2<2, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+            rho = o[0];
+            bnorm2 = o[1];
+        }
+        PMARK(5);
+        set ^= 1;
+        double alpha = 0.0, omega = 1.0, beta = 0.0;
+        bool conv = rho <= atol2 || rho <= rtol2 * bnorm2, pending = false, epi_done = false;
+        int it = 0, maxit_step = 0;
+
+        for (;;) {
+            // ================= phase-1 slot: p update + v = A p  |  epilogue of converged pairs ======
+            if (!conv) {
+                double a[1] = {0.0};
+                double hS[4] = {0.0, 0.0, 0.0, 0.0}, hN[4] = {0.0, 0.0, 0.0, 0.0};
+                if (hs > 0 && own_top && top_valid) {
+                    const long long q = (long long)top_row * nxu + col;
+                    if (it == 0) hS[0] = __ldcg(pBT + q);
+                    else { hS[0] = __ldcg(pS + q); hS[1] = __ldcg(pT + q); hS[2] = __ldcg(pP + q); hS[3] = __ldcg(pV + q); }
+                }
+                if (hs > 0 && own_bot && bot_valid) {
+                    const long long q = (long long)bot_row * nxu + col;
+                    if (it == 0) hN[0] = __ldcg(pBT + q);
+                    else { hN[0] = __ldcg(pS + q); hN[1] = __ldcg(pT + q); hN[2] = __ldcg(pP + q); hN[3] = __ldcg(pV + q); }
+                }
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= hs) continue;
+                    const int i = r * BLOCK3 + tid;
+                    double pn;
+                    if (it == 0) {
+                        pn = sr[r];
+                    } else {
+                        const double rr = sr[r] - omega * t_s[i];
+                        if (pending) x_s[i] += alpha * pp[r] + omega * sr[r];
+                        pn = rr + beta * (pp[r] - omega * v_s[i]);
+                        sr[r] = rr;
+                    }
+                    pp[r] = pn;
+                    put_op(r, pn);
+                }
+                pending = false;
+                const double haloS = it == 0 ? hS[0] : (hS[0] - omega * hS[1]) + beta * (hS[2] - omega * hS[3]);
+                const double haloN = it == 0 ? hN[0] : (hN[0] - omega * hN[1]) + beta * (hN[2] - omega * hN[3]);
+                __syncthreads();
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= hs) continue;
+                    const int si = sidx(r);
+                    const Off o = coef(r);
+                    const double vv = pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, haloN) +
+                                                         o.s * opS(pp, r, haloS));
+                    v_s[r * BLOCK3 + tid] = vv;
+                    a[0] += BT(r) * vv;
+                    const int R = R0 + r;
+                    if (R == 0 || R == h - 1) {
+                        pR[q_of(r)] = sr[r];
+                        pV2[q_of(r)] = vv;
+                    }
+                }
+                block_reduce2<1, 0>(a, red);
+                if (tid == 0) S.part[((long long)set * G + g) * NPART] = a[0];
+                PMARK(1);
+            } else if (!epi_done) {
+                double a[3] = {0.0, 0.0, 0.0};
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= hs) continue;
+                    double dx = X(r);
+                    if (pending) dx += alpha * pp[r] + omega * sr[r];
+                    const long long q = q_of(r);
+                    if (S.mode == 1) S.xptr[me][q] = dx;
+                    else {
+                        pX[q] = dx;
+                        Unew[q] = u_s[uidx(r)] + dx;
+                    }
+                    a[0] += dx * dx;
+                    a[1] = fmax(a[1], fabs(dx));
+                    if (!isfinite(dx)) a[2] = 1.0;
+                }
+                block_reduce2<1, 2>(a, red);
+                if (tid == 0) {
+                    hp[g * 4 + 2] = a[0];
+                    hp[g * 4 + 3] = a[1];
+                    if (a[2] != 0.0) atomicOr(&S.bs->err, 1u);
+                }
+                epi_done = true;
+                pending = false;
+                PMARK(3);
+            }
+            const bool any = bar_sync(S.bs, G, ep, !conv, hi);
+            PMARK(4);
+            if (!any) { set ^= 1; break; }
+            double r0v = 0.0;
+            if (!conv) {
+                double o[1];
+                pair_reduce2<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+                r0v = o[0];
+            }
+            PMARK(5);
+            set ^= 1;
+            if (!conv) {
+                if (r0v == 0.0 || !isfinite(r0v)) {
+                    if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                    conv = true;
+                } else {
+                    alpha = rho / r0v;
+                }
+            }
+            // ================= phase 2: s = r - alpha v, t = A s ====================================
+            if (!conv) {
+                double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // (t,s) (t,t) (b~,s) (b~,t) (s,s)
+                double hS[2] = {0.0, 0.0}, hN[2] = {0.0, 0.0};
+                if (hs > 0 && own_top && top_valid) {
+                    const long long q = (long long)top_row * nxu + col;
+                    hS[0] = __ldcg(pR + q); hS[1] = __ldcg(pV2 + q);
+                }
+                if (hs > 0 && own_bot && bot_valid) {
+                    const long long q = (long long)bot_row * nxu + col;
+                    hN[0] = __ldcg(pR + q); hN[1] = __ldcg(pV2 + q);
+                }
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= hs) continue;
+                    const double s = sr[r] - alpha * v_s[r * BLOCK3 + tid];
+                    sr[r] = s;
+                    put_op(r, s);
+                }
+                const double haloS = hS[0] - alpha * hS[1], haloN = hN[0] - alpha * hN[1];
+                __syncthreads();
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= hs) continue;
+                    const int si = sidx(r);
+                    const Off o = coef(r);
+                    const double s = sr[r];
+                    const double t = s + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(sr, r, haloN) +
+                                                    o.s * opS(sr, r, haloS));
+                    t_s[r * BLOCK3 + tid] = t;
+                    const double b0 = BT(r);
+                    a[0] += t * s; a[1] += t * t; a[2] += b0 * s; a[3] += b0 * t; a[4] += s * s;
+                    const int R = R0 + r;
+                    if (R == 0 || R == h - 1) {
+                        const long long q = q_of(r);
+                        pS[q] = s; pT[q] = t; pP[q] = pp[r]; pV[q] = v_s[r * BLOCK3 + tid];
+                    }
+                }
+                block_reduce2<5, 0>(a, red);
+                if (tid == 0) {
+                    double* pq = S.part + ((long long)set * G + g) * NPART;
+                    for (int j = 0; j < 5; ++j) pq[j] = a[j];
+                }
+                PMARK(2);
+            }
+            bar_sync(S.bs, G, ep, false, hi);
+            PMARK(4);
+            if (!conv) {
+                double o[5];
+                pair_reduce2<5, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+                const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];
+                ++it;
+                pending = true;
+                if (tt2 == 0.0) {
+                    omega = 0.0;
+                    conv = true;
+                } else {
+                    omega = ts / tt2;
+                    const double rhon = r0s - omega * r0t;
+                    const double rn2 = fmax(ss - 2.0 * omega * ts + omega * omega * tt2, 0.0);
+                    if (!isfinite(omega) || !isfinite(rn2)) {
+                        if (tid == 0 && c == 0) atomicOr(&S.bs->err, 1u);
+                        conv = true;
+                    } else if (rn2 <= rtol2 * bnorm2 || rn2 <= atol2 || it >= S.lin_max) {
+                        conv = true;
+                    } else if (omega == 0.0 || rhon == 0.0) {
+                        if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                        conv = true;
+                    } else {
+                        beta = (rhon / rho) * (alpha / omega);
+                        rho = rhon;
+                    }
+                }
+            }
+            set ^= 1;
+            maxit_step = it > maxit_step ? it : maxit_step;
+            PMARK(5);
+        }
+
+        // ---- norms of the finished levels -> per-iteration accumulators; stop rule --------------------
+        const unsigned err = *((volatile unsigned*)&S.bs->err);
+        int stop_status = 2, stop_k = -1;
+        {
+            for (int j = tid; j < G * 4; j += BLOCK3) s_hp_big[j] = __ldcg(hp + j);
+            __syncthreads();
+            const int w = tid >> 5, lane = tid & 31;
+            if (w < A) {
+                const int ga0 = (int)((long long)w * G / A), ga1 = (int)((long long)(w + 1) * G / A);
+                double a4[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int gg = ga0 + lane; gg < ga1; gg += 32) {
+                    a4[0] += s_hp_big[gg * 4 + 0]; a4[1] = fmax(a4[1], s_hp_big[gg * 4 + 1]);
+                    a4[2] += s_hp_big[gg * 4 + 2]; a4[3] = fmax(a4[3], s_hp_big[gg * 4 + 3]);
+                }
+                #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    a4[0] += __shfl_xor_sync(0xffffffffu, a4[0], o);
+                    a4[1] = fmax(a4[1], __shfl_xor_sync(0xffffffffu, a4[1], o));
+                    a4[2] += __shfl_xor_sync(0xffffffffu, a4[2], o);
+                    a4[3] = fmax(a4[3], __shfl_xor_sync(0xffffffffu, a4[3], o));
+                }
+                if (lane == 0) for (int j = 0; j < 4; ++j) red[w * 4 + j] = a4[j];
+            }
+            __syncthreads();
+        }
+        for (int a = 0; a < A; ++a) {
+            const double o[4] = {red[a * 4 + 0], red[a * 4 + 1], red[a * 4 + 2], red[a * 4 + 3]};
+            const int k = ks[a];
+            const int na = S.mode == 1 ? 1 : step - sS[k] + 1;
+            const int sa = k % S.D;
+            if (tid == 0) {
+                if (na == 1) { hacc[sa][0] = hacc[sa][1] = hacc[sa][2] = hacc[sa][3] = 0.0; }
+                hacc[sa][0] += o[0]; hacc[sa][1] = fmax(hacc[sa][1], o[1]);
+                hacc[sa][2] += o[2]; hacc[sa][3] = fmax(hacc[sa][3], o[3]);
+            }
+            __syncthreads();
+            if (S.mode == 0 && na == P.nt) {
+                last_done = k;
+                const double Ntot = (double)ns * (double)P.nt;
+                const double dmax = hacc[sa][3];
+                if (g == 0 && tid == 0) {
+                    S.hist[4 * k + 0] = sqrt(hacc[sa][0] / Ntot);
+                    S.hist[4 * k + 1] = hacc[sa][1];
+                    S.hist[4 * k + 2] = sqrt(hacc[sa][2] / Ntot);
+                    S.hist[4 * k + 3] = dmax;
+                }
+                if (dmax <= S.newton_tol) { stop_status = 0; stop_k = k; }
+                else if (k >= 1 && dmax > 0.5 * prevmax_s && dmax <= 1e3 * S.newton_tol) { stop_status = 1; stop_k = k; }
+                else if (k + 1 >= newton_max) { stop_status = -4; stop_k = k; }
+                __syncthreads();
+                if (tid == 0) prevmax_s = dmax;
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+        if (g == 0 && tid == 0) total_inner += maxit_step;
+        if (c == 0 && tid == 0 && S.stats && S.mode == 0) {
+            atomicAdd((unsigned long long*)&S.stats[4], (unsigned long long)it);
+            atomicAdd((unsigned long long*)&S.stats[8 + kme], (unsigned long long)it);
+        }
+        PMARK(6);
+        if (S.mode == 1) {
+            if (g == 0 && tid == 0) {
+                S.info[0] = maxit_step;
+                S.info[1] = err ? -5 : 0;
+            }
+            flush_prof();
+            return;
+        }
+        if (err && stop_status == 2) { stop_status = -5; stop_k = last_done; }
+        if (stop_status != 2) {
+            const int kf = stop_k + 1;
+            const double* Uf = S.U + (long long)(kf % S.B) * P.nt * ns;
+            const long long N = ns * P.nt;
+            if (S.u_out)
+                for (long long q = (long long)g * BLOCK3 + tid; q < N; q += (long long)G * BLOCK3) S.u_out[q] = __ldcg(Uf + q);
+            if (g == 0 && tid == 0) {
+                S.info[0] = kf;
+                S.info[1] = stop_status;
+                if (S.stats) { S.stats[0] = step; S.stats[1] = total_inner; S.stats[2] = S.D; S.stats[3] = G; }
+            }
+            flush_prof();
+            return;
+        }
+    }
+}
+
+#undef PMARK
+
+}  // namespace pit

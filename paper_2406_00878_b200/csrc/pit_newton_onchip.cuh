@@ -26,6 +26,8 @@ constexpr int NWARP2 = BLOCK2 / 32;
 
 template <int NS, int NM>
 __device__ __forceinline__ void block_reduce2(double (&a)[NS + NM], double* sm) {
+    // butterfly inside each warp, then warp 0 combines the NWARP2 per-warp values with a second (fixed)
+    // butterfly: no serial loop over warps.  Result valid in thread 0.
     constexpr int N = NS + NM;
     #pragma unroll
     for (int i = 0; i < N; ++i)
@@ -39,12 +41,16 @@ __device__ __forceinline__ void block_reduce2(double (&a)[NS + NM], double* sm) 
         #pragma unroll
         for (int i = 0; i < N; ++i) sm[w * N + i] = a[i];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (w == 0) {
         #pragma unroll
         for (int i = 0; i < N; ++i) {
-            double s = sm[i];
-            for (int k = 1; k < NWARP2; ++k) s = i < NS ? s + sm[k * N + i] : fmax(s, sm[k * N + i]);
-            a[i] = s;
+            double v = l < NWARP2 ? sm[l * N + i] : (i < NS ? 0.0 : 0.0);
+            #pragma unroll
+            for (int o = NWARP2 / 2; o > 0; o >>= 1) {
+                const double y = __shfl_xor_sync(0xffffffffu, v, o);
+                v = i < NS ? v + y : fmax(v, y);
+            }
+            a[i] = v;
         }
     }
     __syncthreads();
@@ -137,18 +143,6 @@ __device__ __forceinline__ double node_ext(const Prob& P, const double* __restri
     return __ldcg(ringn + 2 * nxp + (P.ny - 1) + gr);                  // right, (nx, gr+1)
 }
 
-// Optional cycle accounting (S.trace != nullptr, env PIT_TRACE=1): per-CTA clock64 time per category,
-// summed over CTAs: 0 prologue, 1 phase-1 work, 2 phase-2 work, 3 epilogue, 4 grid barriers,
-// 5 scalar reductions after barriers, 6 end-of-step bookkeeping.
-#define PMARK(cat)                                                       \
-    do {                                                                 \
-        if (TRACE) {                                                     \
-            const long long t_ = clock64();                              \
-            prof[cat] += t_ - t_last;                                    \
-            t_last = t_;                                                 \
-        }                                                                \
-    } while (0)
-
 // Off-diagonal Jacobian coefficients for the matvec.  LAW 1 = viscous Burgers with constant viscosity
 // (f = g = u^2/2, mu = m0: a_E = tau (u_E / 2h - mu / h^2), ...), LAW 0 = the general law of Eq. (1).
 template <int LAW>
@@ -164,6 +158,117 @@ __device__ __forceinline__ Off offdiag_law(const Prob& P, const Vals& v) {
     }
     return offdiag(P, v);
 }
+
+// ---- hot per-point loops, as functions with __restrict__ shared-memory operands (the strip arrays are
+// disjoint regions of one dynamic shared buffer; without the qualifier every store would fence the next
+// point's loads) ----------------------------------------------------------------------------------------
+template <int LAW>
+__device__ __forceinline__ double scaled_matvec(const Prob& P, int c0, int l, int W, const double* __restrict__ u_s,
+                                                const double* __restrict__ op_s, const double* __restrict__ ci_s) {
+    const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
+    const Off o = offdiag_law<LAW>(P, uv);
+    return op_s[c0] + ci_s[l] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] + o.s * op_s[c0 - W]);
+}
+
+// phase 1, own points: r = s - omega t, x += alpha p + omega s (pending), p = r + beta (p - omega v)
+template <int PPT>
+__device__ __forceinline__ void p_update(int tid, int W, const int (&lrr)[PPT], double (&x)[PPT], double (&sr)[PPT],
+                                         const double (&bt)[PPT], bool first, bool pending, double alpha, double omega,
+                                         double beta, double* __restrict__ p_s, const double* __restrict__ v_s,
+                                         const double* __restrict__ t_s, double* __restrict__ op_s) {
+    #pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+        const int l = tid + m * BLOCK2;
+        const int lr = lrr[m];
+        if (lr < 0) continue;
+        double pn;
+        if (first) {
+            pn = bt[m];
+        } else {
+            const double pold = p_s[l];
+            const double r = sr[m] - omega * t_s[l];
+            if (pending) x[m] += alpha * pold + omega * sr[m];
+            pn = r + beta * (pold - omega * v_s[l]);
+            sr[m] = r;
+        }
+        p_s[l] = pn;
+        op_s[l + 2 * lr + W + 1] = pn;
+    }
+}
+
+// phase 1 matvec pass (interior rows, or the two boundary rows): v = D^{-1} A p, (b~, v), publish r, v
+template <int PPT, int LAW>
+__device__ __forceinline__ void v_pass(bool boundary, const Prob& P, int tid, int h, int W, const int (&lrr)[PPT],
+                                       const double (&bt)[PPT], const double (&sr)[PPT], long long qbase,
+                                       const double* __restrict__ u_s, const double* __restrict__ op_s,
+                                       const double* __restrict__ ci_s, double* __restrict__ v_s,
+                                       double* __restrict__ pR, double* __restrict__ pV2, double& acc) {
+    #pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+        const int l = tid + m * BLOCK2;
+        const int lr = lrr[m];
+        if (lr < 0 || (lr == 0 || lr == h - 1) != boundary) continue;
+        const double vv = scaled_matvec<LAW>(P, l + 2 * lr + W + 1, l, W, u_s, op_s, ci_s);
+        v_s[l] = vv;
+        acc += bt[m] * vv;
+        if (boundary) {
+            pR[qbase + l] = sr[m];
+            pV2[qbase + l] = vv;
+        }
+    }
+}
+
+// phase 2, own points: s = r - alpha v
+template <int PPT>
+__device__ __forceinline__ void s_update(int tid, int W, const int (&lrr)[PPT], double (&sr)[PPT], double alpha,
+                                         const double* __restrict__ v_s, double* __restrict__ op_s) {
+    #pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+        const int l = tid + m * BLOCK2;
+        const int lr = lrr[m];
+        if (lr < 0) continue;
+        const double s = sr[m] - alpha * v_s[l];
+        sr[m] = s;
+        op_s[l + 2 * lr + W + 1] = s;
+    }
+}
+
+// phase 2 matvec pass: t = D^{-1} A s, the five dots, publish s, t, p, v of the boundary rows
+template <int PPT, int LAW>
+__device__ __forceinline__ void t_pass(bool boundary, const Prob& P, int tid, int h, int W, const int (&lrr)[PPT],
+                                       const double (&bt)[PPT], const double (&sr)[PPT], long long qbase,
+                                       const double* __restrict__ u_s, const double* __restrict__ op_s,
+                                       const double* __restrict__ ci_s, double* __restrict__ t_s,
+                                       const double* __restrict__ p_s, const double* __restrict__ v_s,
+                                       double* __restrict__ pS, double* __restrict__ pT, double* __restrict__ pP,
+                                       double* __restrict__ pV, double (&a)[5]) {
+    #pragma unroll
+    for (int m = 0; m < PPT; ++m) {
+        const int l = tid + m * BLOCK2;
+        const int lr = lrr[m];
+        if (lr < 0 || (lr == 0 || lr == h - 1) != boundary) continue;
+        const double s = sr[m];
+        const double t = scaled_matvec<LAW>(P, l + 2 * lr + W + 1, l, W, u_s, op_s, ci_s);
+        t_s[l] = t;
+        a[0] += t * s; a[1] += t * t; a[2] += bt[m] * s; a[3] += bt[m] * t; a[4] += s * s;
+        if (boundary) {
+            const long long q = qbase + l;
+            pS[q] = s; pT[q] = t; pP[q] = p_s[l]; pV[q] = v_s[l];
+        }
+    }
+}
+
+// Optional cycle accounting (S.trace != nullptr, env PIT_TRACE=1): per-CTA clock64 time per category,
+// summed over CTAs: 0 prologue, 1 phase-1 work, 2 phase-2 work, 3 epilogue, 4 grid barriers,
+// 5 scalar reductions after barriers, 6 end-of-step bookkeeping.
+#define PMARK(cat)                                                       \
+    do {                                                                 \
+        if (TRACE) {                                                     \
+            const long long t_ = clock64();                              \
+            prof[cat] += t_ - t_last;                                    \
+            t_last = t_;                                                 \
+        }                                                                \
+    } while (0)
 
 template <int PPT, bool TRACE, int LAW>
 __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
@@ -211,7 +316,8 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
     const int newton_max = S.mode == 0 ? S.newton_max : 1;
     int set = 0, klo = 0, last_done = -1;
     long long total_inner = 0;
-    const double rtol2 = S.lin_rtol * S.lin_rtol, atol2 = S.lin_atol * S.lin_atol;
+    const double rtol2 = S.lin_rtol * S.lin_rtol;
+    const double atol2 = S.lin_atol * S.lin_atol * (double)P.ns;     // lin_atol bounds the RMS residual
 
     for (int step = 1;; ++step) {
         while (klo < newton_max && step > sS[klo] + P.nt - 1) ++klo;
@@ -252,12 +358,11 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
         const long long qbase = (long long)r0 * nxu;   // global index of point m = qbase + l
 
         // ---- prologue: stage u, fused residual + Jacobian diagonal (kernel a), carry, scaling ----
-        // u rows r0-1 .. r1 staged with cp.async (all of a thread's loads in flight at once); values
-        // outside the domain (Dirichlet ring / zero) are plain stores
+        // Every global read of the prologue is issued before the first wait: u rows r0-1 .. r1 by cp.async,
+        // u^{n-1} and the carry of the own points and the carry halo rows into registers.
+        const bool x0c = S.x0carry && S.mode == 0 && n > 1;
         for (int idx = tid; idx < (h + 2) * W; idx += BLOCK2) {
             const int srow = idx / W, scol = idx - srow * W;
-            op_s[idx] = 0.0;                      // Dirichlet halo of the operand stays 0 (dropped columns)
-            if (h == 0) continue;
             int gr = r0 - 1 + srow, gc = scol - 1;
             bool inside = true;
             if (P.bc == 1) {
@@ -265,6 +370,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 gc = gc < 0 ? gc + nxu : (gc >= nxu ? gc - nxu : gc);
             } else {
                 inside = gr >= 0 && gr < nyu && gc >= 0 && gc < nxu;
+                if (scol == 0 || scol == W - 1) op_s[idx] = 0.0;   // Dirichlet: dropped columns stay 0
             }
             if (inside) {
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(u_s + idx);
@@ -274,13 +380,18 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                 u_s[idx] = node_ext(P, Ulev, ringn, r0 - 1 + srow, scol - 1);
             }
         }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-        const bool x0c = S.x0carry && S.mode == 0 && n > 1;
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        double xh[2] = {0.0, 0.0};                 // carry on the halo rows (x0 = du^{n-1} operand)
+        #pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int idx = tid + j * BLOCK2;
+            if (x0c && h > 0 && idx < 2 * nxu) {
+                const int side = idx >= nxu, col = side ? idx - nxu : idx;
+                if (side ? bot_valid : top_valid) xh[j] = __ldcg(pX + (long long)(side ? bot_row : top_row) * nxu + col);
+            }
+        }
         {
             double a[4] = {0.0, 0.0, 0.0, 0.0};  // sum r0^2, sum r^2, sum b~^2 | max |r|   (r0 = b~ - A~ x0)
-            // issue every global load of the thread first (u^{n-1} and the carry; b in mode 1) so their
-            // latencies overlap, then compute
             #pragma unroll
             for (int m = 0; m < PPT; ++m) {
                 const long long q = qbase + tid + m * BLOCK2;
@@ -294,6 +405,8 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                     }
                 }
             }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
             #pragma unroll
             for (int m = 0; m < PPT; ++m) {
                 const int l = tid + m * BLOCK2;
@@ -324,12 +437,13 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
             if (x0c) {
                 // r0 = b~ - A~ x0 with x0 = du^{n-1}: the operand halo rows are the carry of the
                 // neighbouring strips (written for every point by the previous step's epilogue)
-                for (int idx = tid; idx < 2 * nxu; idx += BLOCK2) {
-                    const int side = idx >= nxu, col = side ? idx - nxu : idx;
-                    double val = 0.0;
-                    if (h > 0 && (side ? bot_valid : top_valid))
-                        val = __ldcg(pX + (long long)(side ? bot_row : top_row) * nxu + col);
-                    op_s[(side ? h + 1 : 0) * W + col + 1] = val;
+                #pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int idx = tid + j * BLOCK2;
+                    if (h > 0 && idx < 2 * nxu) {
+                        const int side = idx >= nxu, col = side ? idx - nxu : idx;
+                        op_s[(side ? h + 1 : 0) * W + col + 1] = xh[j];
+                    }
                 }
                 __syncthreads();
                 if (P.bc == 1)
@@ -380,6 +494,21 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
         bool conv = rho <= atol2 || rho <= rtol2 * bnorm2, pending = false, epi_done = false;
         int it = 0, maxit_step = 0;
 
+        // periodic halo columns of the strip's own rows (the halo rows' wrap cells are never read)
+        auto fill_wrap_own = [&]() {
+            if (P.bc == 1)
+                for (int rr = 1 + tid; rr <= h; rr += BLOCK2) {
+                    op_s[rr * W] = op_s[rr * W + nxu];
+                    op_s[rr * W + nxu + 1] = op_s[rr * W + 1];
+                }
+        };
+        // scaled matvec (D^{-1} A op) at own point l of strip row lr; A_n recomputed from the staged u
+        auto matvec_at = [&](int l, int lr) -> double {
+            const int c0 = l + 2 * lr + W + 1;
+            const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
+            const Off o = offdiag_law<LAW>(P, uv);
+            return op_s[c0] + ci_s[l] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] + o.s * op_s[c0 - W]);
+        };
         // operand halo rows + periodic halo columns, then the scaled matvec y = D^{-1} A op at own points
         auto fill_wrap = [&]() {
             if (P.bc == 1)
@@ -413,26 +542,17 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                         }
                     }
                 }
-                #pragma unroll
-                for (int m = 0; m < PPT; ++m) {
-                    const int l = tid + m * BLOCK2;
-                    if (lrr[m] >= 0) {
-                        const int lr = lrr[m];
-                        const int i = l;
-                        double pn;
-                        if (it == 0) {
-                            pn = bt[m];
-                        } else {
-                            const double r = sr[m] - omega * t_s[i];
-                            if (pending) x[m] += alpha * p_s[i] + omega * sr[m];
-                            pn = r + beta * (p_s[i] - omega * v_s[i]);
-                            sr[m] = r;
-                        }
-                        p_s[i] = pn;
-                        op_s[l + 2 * lr + W + 1] = pn;
-                    }
-                }
+                p_update<PPT>(tid, W, lrr, x, sr, bt, it == 0, pending, alpha, omega, beta, p_s, v_s, t_s, op_s);
                 pending = false;
+                __syncthreads();
+                fill_wrap_own();
+                __syncthreads();
+                // interior rows first: their neighbours are all local, so the L2 latency of the halo loads
+                // issued at the top of the phase is hidden behind this pass
+                auto vpass = [&](bool boundary) {
+                    v_pass<PPT, LAW>(boundary, P, tid, h, W, lrr, bt, sr, qbase, u_s, op_s, ci_s, v_s, pR, pV2, a[0]);
+                };
+                vpass(false);
                 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                     const int idx = tid + j * BLOCK2;
@@ -444,29 +564,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                     }
                 }
                 __syncthreads();
-                fill_wrap();
-                __syncthreads();
-                #pragma unroll
-                for (int m = 0; m < PPT; ++m) {
-                    const int l = tid + m * BLOCK2;
-                    if (lrr[m] >= 0) {
-                        const int lr = lrr[m];
-                        const int i = l;
-                        const int c0 = l + 2 * lr + W + 1;
-                        const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
-                        const Off o = offdiag_law<LAW>(P, uv);
-                        const double pn = op_s[c0];
-                        const double vv = pn + ci_s[i] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] +
-                                                          o.s * op_s[c0 - W]);
-                        v_s[i] = vv;
-                        a[0] += bt[m] * vv;
-                        if (lr == 0 || lr == h - 1) {
-                            const long long q = qbase + l;
-                            pR[q] = sr[m];
-                            pV2[q] = vv;
-                        }
-                    }
-                }
+                vpass(true);
                 block_reduce2<1, 0>(a, red);
                 if (tid == 0) S.part[((long long)set * G + g) * NPART] = a[0];
                 PMARK(1);
@@ -537,16 +635,15 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                         }
                     }
                 }
-                #pragma unroll
-                for (int m = 0; m < PPT; ++m) {
-                    const int l = tid + m * BLOCK2;
-                    if (lrr[m] >= 0) {
-                        const int lr = lrr[m];
-                        const double s = sr[m] - alpha * v_s[l];
-                        sr[m] = s;
-                        op_s[l + 2 * lr + W + 1] = s;
-                    }
-                }
+                s_update<PPT>(tid, W, lrr, sr, alpha, v_s, op_s);
+                __syncthreads();
+                fill_wrap_own();
+                __syncthreads();
+                auto tpass = [&](bool boundary) {
+                    t_pass<PPT, LAW>(boundary, P, tid, h, W, lrr, bt, sr, qbase, u_s, op_s, ci_s, t_s, p_s, v_s, pS, pT, pP,
+                                     pV, a);
+                };
+                tpass(false);
                 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                     const int idx = tid + j * BLOCK2;
@@ -556,28 +653,7 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
                     }
                 }
                 __syncthreads();
-                fill_wrap();
-                __syncthreads();
-                #pragma unroll
-                for (int m = 0; m < PPT; ++m) {
-                    const int l = tid + m * BLOCK2;
-                    if (lrr[m] >= 0) {
-                        const int lr = lrr[m];
-                        const int i = l;
-                        const int c0 = l + 2 * lr + W + 1;
-                        const Vals uv = {u_s[c0], u_s[c0 + 1], u_s[c0 - 1], u_s[c0 + W], u_s[c0 - W]};
-                        const Off o = offdiag_law<LAW>(P, uv);
-                        const double s = sr[m];
-                        const double t = s + ci_s[i] * (o.e * op_s[c0 + 1] + o.w * op_s[c0 - 1] + o.n * op_s[c0 + W] +
-                                                        o.s * op_s[c0 - W]);
-                        t_s[i] = t;
-                        a[0] += t * s; a[1] += t * t; a[2] += bt[m] * s; a[3] += bt[m] * t; a[4] += s * s;
-                        if (lr == 0 || lr == h - 1) {
-                            const long long q = qbase + l;
-                            pS[q] = s; pT[q] = t; pP[q] = p_s[i]; pV[q] = v_s[i];
-                        }
-                    }
-                }
+                tpass(true);
                 block_reduce2<5, 0>(a, red);
                 if (tid == 0) {
                     double* pp = S.part + ((long long)set * G + g) * NPART;
@@ -679,6 +755,10 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
         }
         __syncthreads();
         if (g == 0 && tid == 0) total_inner += maxit_step;
+        if (c == 0 && tid == 0 && S.stats && S.mode == 0) {          // per-pair iteration accounting
+            atomicAdd((unsigned long long*)&S.stats[4], (unsigned long long)it);
+            atomicAdd((unsigned long long*)&S.stats[8 + kme], (unsigned long long)it);
+        }
         PMARK(6);
         if (S.mode == 1) {
             if (g == 0 && tid == 0) {
@@ -706,6 +786,5 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
     }
 }
 
-#undef PMARK
 
 }  // namespace pit

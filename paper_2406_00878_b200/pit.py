@@ -158,14 +158,17 @@ class Solver:
                                                            _stream(stream)))
 
     def stats(self):
-        out = (C.c_int64 * 16)()
-        self._check(lib().pit_stats(self.h, out, 16))
+        out = (C.c_int64 * (17 + 256 + 4))()
+        self._check(lib().pit_stats(self.h, out, 17 + 256 + 4))
         d = {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
              "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6, "engine": out[7],
-             "product_form": bool(out[15])}
+             "product_form": bool(out[15]), "pair_iterations": out[16],
+             "iterations_per_newton_k": [out[17 + k] for k in range(256) if out[17 + k]]}
         if any(out[8:15]):
             names = ["prologue", "phase1", "phase2", "epilogue", "barrier", "reduce", "step_tail"]
             d["trace_cycles_per_cta"] = {k: out[8 + i] / max(1, out[3]) for i, k in enumerate(names)}
+            sub = ["pro_issue", "pro_wait", "pro_residual", "pro_x0mv"]
+            d["trace_cycles_per_cta"].update({k: out[273 + i] / max(1, out[3]) for i, k in enumerate(sub)})
         return d
 
     def sizes(self):

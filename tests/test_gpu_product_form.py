@@ -21,7 +21,7 @@ def _window_case(p, s0, L, seed):
     U = np.tile(p.u0, (p.nt, 1)) + 0.05 * rng.standard_normal((p.nt, p.ns))
     R = O.spacetime_residual(p, U)
     carry = None if s0 == 1 else 0.01 * rng.standard_normal(p.ns)
-    s = pit.Solver(p)
+    s = pit.Solver(p, lin_rtol=1e-13)
     try:
         dU = torch.zeros((L, p.ns), dtype=torch.float64, device="cuda")
         info = torch.zeros(2, dtype=torch.int32, device="cuda")
@@ -62,12 +62,12 @@ def test_product_window_matches_dense_theorem1(case):
 
 def test_auto_selects_product_form_on_c1_and_matches_oracle():
     p = W.config(1)
-    U, hist, nit, st, stats = gpu_solve(p)
+    U, hist, nit, st, stats = gpu_solve(p, lin_rtol=1e-13)
     assert stats["product_form"], "c1's whole horizon is inside the Section 7 gate: AUTO must run Theorem 1"
     assert st in (0, 1)
     seq = O.solve_sequential(p)
     assert normwise_rel(U, seq.U) <= 1e-10
-    Ur, hr, nr, sr, str_ = gpu_solve(p, inverse_mode=pit.PIT_INV_RECURRENCE)
+    Ur, hr, nr, sr, str_ = gpu_solve(p, inverse_mode=pit.PIT_INV_RECURRENCE, lin_rtol=1e-13)
     assert not str_["product_form"]
     assert nr == nit
     assert normwise_rel(U, Ur) <= 1e-13

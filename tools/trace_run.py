@@ -19,6 +19,6 @@ for c in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 5]:
     st = s.stats()
     tr = st.get("trace_cycles_per_cta", {})
     tot = sum(tr.values()) or 1
-    print(f"c{c}: {st['newton_kernel_ms']:.2f} ms, steps {st['steps']}, inner {st['inner_iterations']}, depth {st['depth']}, engine {st['engine']}")
+    print(f"c{c}: {st['newton_kernel_ms']:.2f} ms, steps {st['steps']}, inner(max) {st['inner_iterations']}, pair-sum {st['pair_iterations']}, per-k {st['iterations_per_newton_k']}, depth {st['depth']}")
     print("   " + ", ".join(f"{k} {v / 1e6:.2f}Mcyc ({100 * v / tot:.0f}%)" for k, v in tr.items()))
     s.close()
