@@ -25,8 +25,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     const int W = nxu + 2;
     const int HM = S.hmax;
     double* const u_s = smem;                          // [HM+2][W] u of the strip rows + halo rows (+ ring / wrap columns)
-    double* const op_s = u_s + (HM + 2) * W;           // [HM][W] matvec operand (E/W exchange)
-    double* const v_s = op_s + HM * W;                 // [RMAX][BLOCK3]
+    double* const op_s = u_s + (HM + 2) * W;           // [HM+2][W] matvec operand (E/W exchange, halo rows)
+    double* const v_s = op_s + (HM + 2) * W;           // [RMAX][BLOCK3]
     double* const t_s = v_s + RMAX * BLOCK3;           // [RMAX][BLOCK3]
     double* const x_s = t_s + RMAX * BLOCK3;           // [RMAX][BLOCK3] BiCGSTAB iterate (-> du^n)
     double* const bt_s = x_s + RMAX * BLOCK3;          // [RMAX][BLOCK3] shadow residual r^0 (and b~)
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         const int top_row = r0 == 0 ? nyu - 1 : r0 - 1, bot_row = r1 == nyu ? 0 : r1;
         const long long qc = (long long)(r0 + R0) * nxu + col;      // global index of the sub-strip's first point
         auto q_of = [&](int r) { return qc + (long long)r * nxu; };
-        auto sidx = [&](int r) { return (R0 + r) * W + col + 1; };   // op_s index of own point r
+        auto sidx = [&](int r) { return (R0 + r + 1) * W + col + 1; };   // op_s index of own point r
         auto uidx = [&](int r) { return (R0 + r + 1) * W + col + 1; };   // u_s index of own point r
 
         double sr[RMAX], pp[RMAX];
@@ -107,12 +107,15 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         auto BT = [&](int r) -> double& { return bt_s[r * BLOCK3 + tid]; };
 
         // ---- prologue -----------------------------------------------------------------------------
+        // Fused with iteration 0's first half: the residual + Jacobian diagonal (kernel a), the carry,
+        // r0 = b~ - A~ x0 (x0 = du^{n-1}), and v0 = A~ p0 with p0 = r0 are all formed before the first grid
+        // barrier.  r0 on the two halo rows (needed by v0) is recomputed redundantly by the edge threads from
+        // u (two rows deep), u^{n-1} and the carry, all of which are inputs of this step.
         const bool x0c = S.x0carry && S.mode == 0 && n > 1;
-        double xhS = 0.0, xhN = 0.0;          // carry across the CTA boundary rows (x0 operand)
+        const bool hasS = hs > 0 && own_top && top_valid, hasN = hs > 0 && own_bot && bot_valid;
         double up[RMAX];
-        // stage u of the own column, rows -1 .. hs (the sub-strip plus one row each side), with the E/W halo
-        // columns (periodic wrap copy or Dirichlet ring) written by the edge columns
-        // (cp.async for values inside the domain, so all of a thread's row loads are in flight at once)
+        // stage u of the own column, rows -1 .. hs, with the E/W halo columns (periodic wrap or Dirichlet
+        // ring) written by the edge columns (cp.async for values inside the domain: all loads in flight)
         auto stage_u = [&](int ui, int gr, int gc) {
             bool inside = true;
             if (P.bc == 1) {
@@ -138,6 +141,14 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (col == nxu - 1) stage_u(ui + 1, gr, nxu);       // E halo column
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
+        auto rowq = [&](int gr) -> long long {                    // global index of (row gr, col), wrapped
+            gr = gr < 0 ? gr + nyu : (gr >= nyu ? gr - nyu : gr);
+            return (long long)gr * nxu + col;
+        };
+        auto carry_at = [&](int gr) -> double {                   // du^{n-1} at (gr, col); 0 outside (Dirichlet)
+            if (S.mode == 1 || n == 1 || (P.bc != 1 && (gr < 0 || gr >= nyu))) return 0.0;
+            return __ldcg(pX + rowq(gr));
+        };
         #pragma unroll
         for (int r = 0; r < RMAX; ++r) {
             up[r] = 0.0; sr[r] = 0.0;
@@ -148,15 +159,24 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     up[r] = __ldcg(uprev + q_of(r));
                     sr[r] = n == 1 ? 0.0 : __ldcg(pX + q_of(r));
                 }
-                if (P.bc != 1) {
-                    if (col == 0) op_s[sidx(r) - 1] = 0.0;
-                    if (col == nxu - 1) op_s[sidx(r) + 1] = 0.0;
-                }
             }
         }
-        if (x0c && hs > 0) {
-            if (own_top && top_valid) xhS = __ldcg(pX + (long long)top_row * nxu + col);
-            if (own_bot && bot_valid) xhN = __ldcg(pX + (long long)bot_row * nxu + col);
+        // halo-point inputs: S halo (row r0-1) and N halo (row r1) of this column
+        double hS_u2 = 0.0, hS_up = 0.0, hS_x = 0.0, hS_x2 = 0.0, hS_b = 0.0;
+        double hN_u2 = 0.0, hN_up = 0.0, hN_x = 0.0, hN_x2 = 0.0, hN_b = 0.0;
+        if (hasS) {
+            hS_u2 = node_ext(P, Ulev, ringn, r0 - 2, col);
+            if (S.mode == 1) hS_b = __ldcg(S.bptr[me] + rowq(r0 - 1));
+            else hS_up = (n == 1 ? S.u0 : uprev)[rowq(r0 - 1)];
+            hS_x = carry_at(r0 - 1);                                     // carry (enters b~)
+            hS_x2 = x0c ? carry_at(r0 - 2) : 0.0;                        // x0 one row further
+        }
+        if (hasN) {
+            hN_u2 = node_ext(P, Ulev, ringn, r1 + 1, col);
+            if (S.mode == 1) hN_b = __ldcg(S.bptr[me] + rowq(r1));
+            else hN_up = (n == 1 ? S.u0 : uprev)[rowq(r1)];
+            hN_x = carry_at(r1);
+            hN_x2 = x0c ? carry_at(r1 + 1) : 0.0;
         }
         PMARK(7);
         asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -172,22 +192,26 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (r > 0) return o[r - 1];
             return own_top ? haloS : op_s[sidx(r) - W];
         };
-        auto put_op = [&](int r, double val) {
-            const int si = sidx(r);
+        auto put_op_at = [&](int si, double val) {
             op_s[si] = val;
             if (P.bc == 1) {
                 if (col == 0) op_s[si + nxu] = val;
                 if (col == nxu - 1) op_s[si - nxu] = val;
+            } else {
+                if (col == 0) op_s[si - 1] = 0.0;          // Dirichlet: the dropped columns stay 0
+                if (col == nxu - 1) op_s[si + 1] = 0.0;
             }
         };
+        auto put_op = [&](int r, double val) { put_op_at(sidx(r), val); };
         auto coef = [&](int r) -> Off {
             const int ui = uidx(r);
             const Vals uv = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], u_s[ui - W]};
             return offdiag_law<LAW>(P, uv);
         };
         auto cinv = [&](int r) -> double { return LAW == 1 ? ci_const : ci_s[r * BLOCK3 + tid]; };
+        double hS_r0 = 0.0, hN_r0 = 0.0;       // r0 = p0 on the halo rows
         {
-            double a[4] = {0.0, 0.0, 0.0, 0.0};  // sum r0^2, sum r^2, sum b~^2 | max |r|
+            double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // sum r0^2, sum r^2, sum b~^2, sum r0 v0 | max |r|
             #pragma unroll
             for (int r = 0; r < RMAX; ++r) {
                 pp[r] = 0.0;
@@ -201,7 +225,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 } else {
                     const double res = -o.G;
                     a[1] += res * res;
-                    a[3] = fmax(a[3], fabs(res));
+                    a[4] = fmax(a[4], fabs(res));
                     rhs = res + sr[r];                 // r^n + du^{n-1}  (row n of Eq. 7)
                 }
                 const double ci = 1.0 / o.aC;
@@ -210,54 +234,121 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 X(r) = x0;
                 sr[r] = rhs * ci;                      // b~ (r0 once the x0 matvec is subtracted)
                 a[2] += sr[r] * sr[r];
-                if (x0c) { pp[r] = x0; put_op(r, x0); }
+                pp[r] = x0;
+                put_op(r, x0);
+            }
+            // b~ - diag part on the halo points (u stencil: own column rows from u_s, the far row in a register)
+            double hS_ci = 0.0, hN_ci = 0.0, hS_bt = 0.0, hN_bt = 0.0;
+            Off hS_o = {0.0, 0.0, 0.0, 0.0}, hN_o = {0.0, 0.0, 0.0, 0.0};
+            if (hasS) {
+                const int ui = uidx(-1);
+                const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], hS_u2};
+                const RJ o = residual_jacobian_raw(P, v, hS_up);
+                hS_ci = 1.0 / o.aC;
+                hS_bt = ((S.mode == 1 ? hS_b : -o.G + (n == 1 ? 0.0 : hS_x))) * hS_ci;
+                hS_o = offdiag_law<LAW>(P, v);
+                put_op_at(sidx(-1), x0c ? hS_x : 0.0);
+            }
+            if (hasN) {
+                const int ui = uidx(hs);
+                const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], hN_u2, u_s[ui - W]};
+                const RJ o = residual_jacobian_raw(P, v, hN_up);
+                hN_ci = 1.0 / o.aC;
+                hN_bt = ((S.mode == 1 ? hN_b : -o.G + (n == 1 ? 0.0 : hN_x))) * hN_ci;
+                hN_o = offdiag_law<LAW>(P, v);
+                put_op_at(sidx(hs), x0c ? hN_x : 0.0);
             }
             PMARK(9);
-            if (x0c) {
-                __syncthreads();
-                #pragma unroll
-                for (int r = 0; r < RMAX; ++r) {
-                    if (r >= hs) continue;
-                    const int si = sidx(r);
-                    const Off o = coef(r);
-                    sr[r] -= pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, xhN) +
-                                                o.s * opS(pp, r, xhS));
-                }
+            __syncthreads();                           // op_s holds x0 on own rows + halo rows
+            // r0 = b~ - A~ x0 on own points and on the halo points
+            #pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+                if (r >= hs || !x0c) continue;
+                const int si = sidx(r);
+                const Off o = coef(r);
+                sr[r] -= pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, hN_x) +
+                                            o.s * opS(pp, r, hS_x));     // x0c: hN_x/hS_x = x0 on the halo rows
             }
+            if (hasS) {
+                const int si = sidx(-1);
+                hS_r0 = hS_bt - (x0c ? hS_x + hS_ci * (hS_o.e * op_s[si + 1] + hS_o.w * op_s[si - 1] +
+                                                        hS_o.n * (hs > 0 ? pp[0] : 0.0) + hS_o.s * hS_x2)
+                                     : 0.0);
+            }
+            if (hasN) {
+                const int si = sidx(hs);
+                double xN = 0.0;                       // x0 at the last own row (the halo point's S neighbour)
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) if (r == hs - 1) xN = pp[r];
+                hN_r0 = hN_bt - (x0c ? hN_x + hN_ci * (hN_o.e * op_s[si + 1] + hN_o.w * op_s[si - 1] +
+                                                        hN_o.n * hN_x2 + hN_o.s * xN)
+                                     : 0.0);
+            }
+            __syncthreads();                           // all reads of x0 done: op_s <- p0 = r0
             #pragma unroll
             for (int r = 0; r < RMAX; ++r) {
                 if (r >= hs) continue;
                 BT(r) = sr[r];                         // r0, and the BiCGSTAB shadow vector r^0 = r0
+                pp[r] = sr[r];                         // p0 = r0
                 a[0] += sr[r] * sr[r];
+                put_op(r, sr[r]);
+            }
+            __syncthreads();
+            // v0 = A~ p0; publish r0, v0 of the boundary rows (the halo of phase 2)
+            #pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+                if (r >= hs) continue;
+                const int si = sidx(r);
+                const Off o = coef(r);
+                const double vv = pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, hN_r0) +
+                                                     o.s * opS(pp, r, hS_r0));
+                v_s[r * BLOCK3 + tid] = vv;
+                a[3] += sr[r] * vv;
                 const int R = R0 + r;
-                if (R == 0 || R == h - 1) pBT[q_of(r)] = sr[r];
+                if (R == 0 || R == h - 1) {
+                    pR[q_of(r)] = sr[r];
+                    pV2[q_of(r)] = vv;
+                }
             }
             PMARK(10);
-            block_reduce2<3, 1>(a, red);
+            block_reduce2<4, 1>(a, red);
             if (tid == 0) {
-                S.part[((long long)set * G + g) * NPART] = a[0];
-                S.part[((long long)set * G + g) * NPART + 1] = a[2];
+                double* pq = S.part + ((long long)set * G + g) * NPART;
+                pq[0] = a[0];
+                pq[1] = a[2];
+                pq[2] = a[3];
                 hp[g * 4 + 0] = a[1];
-                hp[g * 4 + 1] = a[3];
+                hp[g * 4 + 1] = a[4];
             }
         }
         PMARK(0);
-        bar_sync(S.bs, G, ep, false, hi);
+        bar_sync(S.bs, G, ep, true, hi);
         PMARK(4);
-        double bnorm2, rho;
+        double bnorm2, rho, r0v0;
         {
-            double o[2];
-            pair_reduce2<2, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
-            rho = o[0];
-            bnorm2 = o[1];
+            double o[3];
+            pair_reduce2<3, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+            rho = o[0];                                // (r^0, r0) = ||r0||^2
+            bnorm2 = o[1];                             // ||b~||^2: reference of the relative stopping test
+            r0v0 = o[2];                               // (r^0, v0)
         }
         PMARK(5);
         set ^= 1;
         double alpha = 0.0, omega = 1.0, beta = 0.0;
         bool conv = rho <= atol2 || rho <= rtol2 * bnorm2, pending = false, epi_done = false;
+        if (!conv) {
+            if (r0v0 == 0.0 || !isfinite(r0v0)) {
+                if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                conv = true;
+            } else {
+                alpha = rho / r0v0;
+            }
+        }
         int it = 0, maxit_step = 0;
+        bool fused_first = true;                       // iteration 0's phase 1 happened in the prologue
 
         for (;;) {
+            if (!fused_first) {
             // ================= phase-1 slot: p update + v = A p  |  epilogue of converged pairs ======
             if (!conv) {
                 double a[1] = {0.0};
@@ -356,6 +447,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     alpha = rho / r0v;
                 }
             }
+            }   // !fused_first
+            fused_first = false;
             // ================= phase 2: s = r - alpha v, t = A s ====================================
             if (!conv) {
                 double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // (t,s) (t,t) (b~,s) (b~,t) (s,s)

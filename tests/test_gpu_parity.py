@@ -205,3 +205,19 @@ def test_column_engine(case):
     assert n3 == n1 and normwise_rel(U3, U1) <= 1e-11
     seq = O.solve_sequential(p, levels=m)
     assert np.abs(U3[:m] - seq.U).max() / np.abs(seq.U).max() <= 1e-10
+
+
+@pytest.mark.parametrize("ny,nt,depth", [(8, 3, 0), (8, 2, 1), (16, 3, 0), (148, 3, 0), (300, 3, 0)])
+@pytest.mark.parametrize("nx", [256, 512])
+def test_column_engine_strip_shapes(nx, ny, nt, depth):
+    """Engine 3 with strips of 0, 1, 2, ... rows per CTA (more CTAs than rows, ragged splits, the column
+    groups of nx = 256): identical iterates to the global-state engine."""
+    rng = np.random.default_rng(nx + ny)
+    p = W.custom(f"p{nx}x{ny}", W.BURGERS, W.PERIODIC, nx, ny, nt, 1e-4, 5e-3, 0.0, u0=0.3 * rng.standard_normal(nx * ny))
+    kw = dict(inverse_mode=pit.PIT_INV_RECURRENCE, pipeline_depth=depth, lin_rtol=1e-13)
+    U3, h3, n3, s3, st3 = gpu_solve(p, engine=3, **kw)
+    U1, h1, n1, s1, _ = gpu_solve(p, engine=1, **kw)
+    assert st3["engine"] == 3 and s3 in (0, 1) and n3 == n1
+    assert normwise_rel(U3, U1) <= 1e-13
+    for k in range(n3):
+        assert abs(h3[k, 3] - h1[k, 3]) <= 1e-8 * h1[k, 3] + 1e-2 * p.newton_tol   # + the update rounding floor
