@@ -305,7 +305,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
         (rc = dalloc(h, &h->d_small, 2 * 1024 + 2)) ||
         (rc = dalloc(h, &h->bs, 1)) ||
-        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 11)))) {
+        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 13)))) {
         free_all(h);
         delete h;
         return rc;
@@ -379,7 +379,7 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
         S.bs = h->bs;
         S.trace = h->trace;
         S.x0carry = getenv("PIT_X0") ? atoi(getenv("PIT_X0")) : 1;   // default: start from du^{n-1}
-        if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 11 * sizeof(unsigned long long), st));
+        if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 13 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
         CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
         if (h->engine == 3)
@@ -721,14 +721,14 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
         CUDA_TRY(h, cudaEventElapsedTime(&t_init, h->ev[0], h->ev[1]));
         CUDA_TRY(h, cudaEventElapsedTime(&t_newton, h->ev[2], h->ev[3]));
     }
-    unsigned long long tr[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tr[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (h->trace) CUDA_TRY(h, cudaMemcpy(tr, h->trace, sizeof(tr), cudaMemcpyDeviceToHost));
     const long long v[17] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
                              h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
                              (long long)tr[4], (long long)tr[5], (long long)tr[6], h->product_used ? 1 : 0, s[4]};
     for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];
     for (int i = 17; i < n && i < 17 + MAXK; ++i) out[i] = s[8 + (i - 17)];
-    for (int i = 17 + MAXK; i < n && i < 17 + MAXK + 4; ++i) out[i] = (long long)tr[7 + (i - 17 - MAXK)];
+    for (int i = 17 + MAXK; i < n && i < 17 + MAXK + 6; ++i) out[i] = (long long)tr[7 + (i - 17 - MAXK)];
     return PIT_OK;
 }
 

@@ -51,11 +51,11 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
 
     unsigned ep = 0;
     unsigned hi[2] = {0u, 0u};
-    long long prof[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long t_last = clock64();
     auto flush_prof = [&]() {
         if (TRACE && tid == 0)
-            for (int j = 0; j < 11; ++j) atomicAdd(S.trace + j, (unsigned long long)prof[j]);
+            for (int j = 0; j < 13; ++j) atomicAdd(S.trace + j, (unsigned long long)prof[j]);
     };
     const int newton_max = S.mode == 0 ? S.newton_max : 1;
     int set = 0, klo = 0, last_done = -1;
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ks[A++] = k;
         if (S.mode == 1) { A = S.nb; for (int a = 0; a < A; ++a) ks[a] = a; }
         int me = 0;
-        while (me + 1 < A && (long long)(me + 1) * G / A <= g) ++me;
-        const int g0 = (int)((long long)me * G / A), g1 = (int)((long long)(me + 1) * G / A);
+        while (me + 1 < A && (me + 1) * G / A <= g) ++me;                 // 32-bit: G * A < 2^31
+        const int g0 = me * G / A, g1 = (me + 1) * G / A;
         const int kme = ks[me];
         const int n = S.mode == 1 ? S.blev[me] : step - sS[kme] + 1;
         const int slot = kme % S.D;
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         double* const pS = sl.s;    double* const pT = sl.t;  double* const pP = sl.p[0];  double* const pV = sl.v[0];
         double* const pR = sl.r;    double* const pV2 = sl.v[1];
         const int c = g - g0, C = g1 - g0;
-        const int r0 = (int)((long long)c * nyu / C), r1 = (int)((long long)(c + 1) * nyu / C);
+        const int r0 = c * nyu / C, r1 = (c + 1) * nyu / C;                // 32-bit: C * nyu < 2^31
         const int h = r1 - r0;
         const double* Ulev = S.mode == 1 ? S.U + (long long)(n - 1) * ns : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
         const double* uprev = n == 1 ? S.u0 : Ulev - ns;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         double* Unew = S.mode == 1 ? nullptr : S.U + ((long long)nbuf * P.nt + (n - 1)) * ns;
         double* hp = S.hpart + (long long)(step & 1) * G * 4;
         // this thread's sub-strip of rows [R0, R1) (strip-local), column col
-        const int R0 = (int)((long long)grp * h / Gr), R1 = (int)((long long)(grp + 1) * h / Gr);
+        const int R0 = grp * h / Gr, R1 = (grp + 1) * h / Gr;
         const int hs = R1 - R0;
         const bool own_top = R0 == 0, own_bot = R1 == h;          // sub-strip touches the CTA's halo rows
         const bool top_valid = P.bc == 1 || r0 > 0, bot_valid = P.bc == 1 || r1 < nyu;
@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         auto X = [&](int r) -> double& { return x_s[r * BLOCK3 + tid]; };
         auto BT = [&](int r) -> double& { return bt_s[r * BLOCK3 + tid]; };
 
+        PMARK(11);
         // ---- prologue -----------------------------------------------------------------------------
         // Fused with iteration 0's first half: the residual + Jacobian diagonal (kernel a), the carry,
         // r0 = b~ - A~ x0 (x0 = du^{n-1}), and v0 = A~ p0 with p0 = r0 are all formed before the first grid
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (col == nxu - 1) stage_u(ui + 1, gr, nxu);       // E halo column
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
+        PMARK(12);
         auto rowq = [&](int gr) -> long long {                    // global index of (row gr, col), wrapped
             gr = gr < 0 ? gr + nyu : (gr >= nyu ? gr - nyu : gr);
             return (long long)gr * nxu + col;
@@ -218,17 +220,18 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 if (r >= hs) continue;
                 const int ui = uidx(r);
                 const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], u_s[ui - W]};
-                const RJ o = residual_jacobian_raw(P, v, up[r]);
+                double G, aC;
+                res_diag<LAW>(P, v, up[r], G, aC);
                 double rhs;
                 if (S.mode == 1) {
                     rhs = sr[r];
                 } else {
-                    const double res = -o.G;
+                    const double res = -G;
                     a[1] += res * res;
                     a[4] = fmax(a[4], fabs(res));
                     rhs = res + sr[r];                 // r^n + du^{n-1}  (row n of Eq. 7)
                 }
-                const double ci = 1.0 / o.aC;
+                const double ci = LAW == 1 ? ci_const : 1.0 / aC;
                 if (LAW != 1) ci_s[r * BLOCK3 + tid] = ci;
                 const double x0 = x0c ? sr[r] : 0.0;
                 X(r) = x0;
@@ -243,18 +246,20 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (hasS) {
                 const int ui = uidx(-1);
                 const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], hS_u2};
-                const RJ o = residual_jacobian_raw(P, v, hS_up);
-                hS_ci = 1.0 / o.aC;
-                hS_bt = ((S.mode == 1 ? hS_b : -o.G + (n == 1 ? 0.0 : hS_x))) * hS_ci;
+                double G, aC;
+                res_diag<LAW>(P, v, hS_up, G, aC);
+                hS_ci = LAW == 1 ? ci_const : 1.0 / aC;
+                hS_bt = ((S.mode == 1 ? hS_b : -G + (n == 1 ? 0.0 : hS_x))) * hS_ci;
                 hS_o = offdiag_law<LAW>(P, v);
                 put_op_at(sidx(-1), x0c ? hS_x : 0.0);
             }
             if (hasN) {
                 const int ui = uidx(hs);
                 const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], hN_u2, u_s[ui - W]};
-                const RJ o = residual_jacobian_raw(P, v, hN_up);
-                hN_ci = 1.0 / o.aC;
-                hN_bt = ((S.mode == 1 ? hN_b : -o.G + (n == 1 ? 0.0 : hN_x))) * hN_ci;
+                double G, aC;
+                res_diag<LAW>(P, v, hN_up, G, aC);
+                hN_ci = LAW == 1 ? ci_const : 1.0 / aC;
+                hN_bt = ((S.mode == 1 ? hN_b : -G + (n == 1 ? 0.0 : hN_x))) * hN_ci;
                 hN_o = offdiag_law<LAW>(P, v);
                 put_op_at(sidx(hs), x0c ? hN_x : 0.0);
             }
@@ -553,36 +558,39 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             }
             __syncthreads();
         }
-        for (int a = 0; a < A; ++a) {
-            const double o[4] = {red[a * 4 + 0], red[a * 4 + 1], red[a * 4 + 2], red[a * 4 + 3]};
-            const int k = ks[a];
-            const int na = S.mode == 1 ? 1 : step - sS[k] + 1;
-            const int sa = k % S.D;
-            if (tid == 0) {
+        __shared__ int s_stop[3];                      // stop_status, stop_k, last_done (thread 0 -> all)
+        if (tid == 0) {
+            int st_ = 2, sk_ = -1, ld_ = last_done;
+            for (int a = 0; a < A; ++a) {
+                const double o[4] = {red[a * 4 + 0], red[a * 4 + 1], red[a * 4 + 2], red[a * 4 + 3]};
+                const int k = ks[a];
+                const int na = S.mode == 1 ? 1 : step - sS[k] + 1;
+                const int sa = k % S.D;
                 if (na == 1) { hacc[sa][0] = hacc[sa][1] = hacc[sa][2] = hacc[sa][3] = 0.0; }
                 hacc[sa][0] += o[0]; hacc[sa][1] = fmax(hacc[sa][1], o[1]);
                 hacc[sa][2] += o[2]; hacc[sa][3] = fmax(hacc[sa][3], o[3]);
-            }
-            __syncthreads();
-            if (S.mode == 0 && na == P.nt) {
-                last_done = k;
-                const double Ntot = (double)ns * (double)P.nt;
-                const double dmax = hacc[sa][3];
-                if (g == 0 && tid == 0) {
-                    S.hist[4 * k + 0] = sqrt(hacc[sa][0] / Ntot);
-                    S.hist[4 * k + 1] = hacc[sa][1];
-                    S.hist[4 * k + 2] = sqrt(hacc[sa][2] / Ntot);
-                    S.hist[4 * k + 3] = dmax;
+                if (S.mode == 0 && na == P.nt) {          // iteration k complete: record and test
+                    ld_ = k;
+                    const double Ntot = (double)ns * (double)P.nt;
+                    const double dmax = hacc[sa][3];
+                    if (g == 0) {
+                        S.hist[4 * k + 0] = sqrt(hacc[sa][0] / Ntot);
+                        S.hist[4 * k + 1] = hacc[sa][1];
+                        S.hist[4 * k + 2] = sqrt(hacc[sa][2] / Ntot);
+                        S.hist[4 * k + 3] = dmax;
+                    }
+                    if (dmax <= S.newton_tol) { st_ = 0; sk_ = k; }
+                    else if (k >= 1 && dmax > 0.5 * prevmax_s && dmax <= 1e3 * S.newton_tol) { st_ = 1; sk_ = k; }
+                    else if (k + 1 >= newton_max) { st_ = -4; sk_ = k; }
+                    prevmax_s = dmax;
                 }
-                if (dmax <= S.newton_tol) { stop_status = 0; stop_k = k; }
-                else if (k >= 1 && dmax > 0.5 * prevmax_s && dmax <= 1e3 * S.newton_tol) { stop_status = 1; stop_k = k; }
-                else if (k + 1 >= newton_max) { stop_status = -4; stop_k = k; }
-                __syncthreads();
-                if (tid == 0) prevmax_s = dmax;
-                __syncthreads();
             }
+            s_stop[0] = st_; s_stop[1] = sk_; s_stop[2] = ld_;
         }
         __syncthreads();
+        stop_status = s_stop[0];
+        stop_k = s_stop[1];
+        last_done = s_stop[2];
         if (g == 0 && tid == 0) total_inner += maxit_step;
         if (c == 0 && tid == 0 && S.stats && S.mode == 0) {
             atomicAdd((unsigned long long*)&S.stats[4], (unsigned long long)it);

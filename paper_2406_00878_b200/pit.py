@@ -158,8 +158,8 @@ class Solver:
                                                            _stream(stream)))
 
     def stats(self):
-        out = (C.c_int64 * (17 + 256 + 4))()
-        self._check(lib().pit_stats(self.h, out, 17 + 256 + 4))
+        out = (C.c_int64 * (17 + 256 + 6))()
+        self._check(lib().pit_stats(self.h, out, 17 + 256 + 6))
         d = {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
              "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6, "engine": out[7],
              "product_form": bool(out[15]), "pair_iterations": out[16],
@@ -167,7 +167,7 @@ class Solver:
         if any(out[8:15]):
             names = ["prologue", "phase1", "phase2", "epilogue", "barrier", "reduce", "step_tail"]
             d["trace_cycles_per_cta"] = {k: out[8 + i] / max(1, out[3]) for i, k in enumerate(names)}
-            sub = ["pro_issue", "pro_wait", "pro_residual", "pro_x0mv"]
+            sub = ["pro_loads", "pro_wait", "pro_residual", "pro_x0mv", "step_setup", "pro_stage"]
             d["trace_cycles_per_cta"].update({k: out[273 + i] / max(1, out[3]) for i, k in enumerate(sub)})
         return d
 
