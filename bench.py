@@ -92,6 +92,23 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank time over all ranks (the multi-GPU timing rule); identity without a process group."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(world_size: int, dof_iterations_per_rank: float, seconds_max: float) -> float:
+    """Whole-job value for replicas-only scaling: every rank solves its own copy, so the job
+    processes world_size x the DOF*iterations of one rank in the slowest rank's time."""
+    return world_size * dof_iterations_per_rank / seconds_max
+
+
 def oracle_sample(p, budget_s=15.0, max_levels=None):
     """The oracle (sequential BDF1 + Newton, one core) on a bounded prefix of the workload: levels
     1..L at full spatial size (a prefix is exact by causality).  Returns (value, levels, seconds)."""
@@ -193,13 +210,10 @@ def main():
         barrier()
     elapsed_ms = e0.elapsed_time(e1)
     nit, status = (int(v) for v in d_info.cpu())
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    elapsed_ms = float(t.item())
+    elapsed_ms = max_over_ranks(elapsed_ms, dev)
     ms_per_step = elapsed_ms / args.steps
     dof_it = float(p.dof) * nit
-    value = ws * dof_it / (ms_per_step * 1e-3)
+    value = replica_throughput(ws, dof_it, ms_per_step * 1e-3)
 
     # kernel (a) standalone on the same field (the HBM-streaming stencil the north star names)
     d_R = torch.empty_like(d_out)
@@ -230,10 +244,7 @@ def main():
                          h_out.data_ptr(), h_hist.data_ptr(), pit.C.addressof(nit_c))
         assert rc in (0, 1), rc
     e2e_s = (time.perf_counter() - te) / args.e2e_steps
-    t2 = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = ws * float(p.dof) * nit_c.value / float(t2.item())
+    e2e_value = replica_throughput(ws, float(p.dof) * nit_c.value, max_over_ranks(e2e_s, dev))
 
     if rank != 0:
         if ws > 1:
