@@ -352,148 +352,142 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         int it = 0, maxit_step = 0;
         bool fused_first = true;                       // iteration 0's phase 1 happened in the prologue
 
+        // Control flow around every block / pair reduction is uniform across the CTA (converged pairs reduce
+        // zeros).
         for (;;) {
             if (!fused_first) {
-            // ================= phase-1 slot: p update + v = A p  |  epilogue of converged pairs ======
-            if (!conv) {
-                double a[1] = {0.0};
-                double hS[4] = {0.0, 0.0, 0.0, 0.0}, hN[4] = {0.0, 0.0, 0.0, 0.0};
-                if (hs > 0 && own_top && top_valid) {
-                    const long long q = (long long)top_row * nxu + col;
-                    if (it == 0) hS[0] = __ldcg(pBT + q);
-                    else { hS[0] = __ldcg(pS + q); hS[1] = __ldcg(pT + q); hS[2] = __ldcg(pP + q); hS[3] = __ldcg(pV + q); }
-                }
-                if (hs > 0 && own_bot && bot_valid) {
-                    const long long q = (long long)bot_row * nxu + col;
-                    if (it == 0) hN[0] = __ldcg(pBT + q);
-                    else { hN[0] = __ldcg(pS + q); hN[1] = __ldcg(pT + q); hN[2] = __ldcg(pP + q); hN[3] = __ldcg(pV + q); }
-                }
-                #pragma unroll
-                for (int r = 0; r < RMAX; ++r) {
-                    if (r >= hs) continue;
-                    const int i = r * BLOCK3 + tid;
-                    double pn;
-                    if (it == 0) {
-                        pn = sr[r];
-                    } else {
+                // ============ phase-1 slot: p update + v = A p  |  epilogue of a pair that just converged ======
+                double a[4] = {0.0, 0.0, 0.0, 0.0};        // (b~, v) | sum du^2 | max |du|, nonfinite
+                const bool do_p1 = !conv, do_epi = conv && !epi_done;
+                if (do_p1) {
+                    double hS[4] = {0.0, 0.0, 0.0, 0.0}, hN[4] = {0.0, 0.0, 0.0, 0.0};
+                    if (hasS) {
+                        const long long q = (long long)top_row * nxu + col;
+                        hS[0] = __ldcg(pS + q); hS[1] = __ldcg(pT + q); hS[2] = __ldcg(pP + q); hS[3] = __ldcg(pV + q);
+                    }
+                    if (hasN) {
+                        const long long q = (long long)bot_row * nxu + col;
+                        hN[0] = __ldcg(pS + q); hN[1] = __ldcg(pT + q); hN[2] = __ldcg(pP + q); hN[3] = __ldcg(pV + q);
+                    }
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) {
+                        if (r >= hs) continue;
+                        const int i = r * BLOCK3 + tid;
                         const double rr = sr[r] - omega * t_s[i];
                         if (pending) x_s[i] += alpha * pp[r] + omega * sr[r];
-                        pn = rr + beta * (pp[r] - omega * v_s[i]);
+                        const double pn = rr + beta * (pp[r] - omega * v_s[i]);
                         sr[r] = rr;
+                        pp[r] = pn;
+                        put_op(r, pn);
                     }
-                    pp[r] = pn;
-                    put_op(r, pn);
-                }
-                pending = false;
-                const double haloS = it == 0 ? hS[0] : (hS[0] - omega * hS[1]) + beta * (hS[2] - omega * hS[3]);
-                const double haloN = it == 0 ? hN[0] : (hN[0] - omega * hN[1]) + beta * (hN[2] - omega * hN[3]);
-                __syncthreads();
-                #pragma unroll
-                for (int r = 0; r < RMAX; ++r) {
-                    if (r >= hs) continue;
-                    const int si = sidx(r);
-                    const Off o = coef(r);
-                    const double vv = pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, haloN) +
-                                                         o.s * opS(pp, r, haloS));
-                    v_s[r * BLOCK3 + tid] = vv;
-                    a[0] += BT(r) * vv;
-                    const int R = R0 + r;
-                    if (R == 0 || R == h - 1) {
-                        pR[q_of(r)] = sr[r];
-                        pV2[q_of(r)] = vv;
+                    pending = false;
+                    const double haloS = (hS[0] - omega * hS[1]) + beta * (hS[2] - omega * hS[3]);
+                    const double haloN = (hN[0] - omega * hN[1]) + beta * (hN[2] - omega * hN[3]);
+                    __syncthreads();
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) {
+                        if (r >= hs) continue;
+                        const int si = sidx(r);
+                        const Off o = coef(r);
+                        const double vv = pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] +
+                                                             o.n * opN(pp, r, haloN) + o.s * opS(pp, r, haloS));
+                        v_s[r * BLOCK3 + tid] = vv;
+                        a[0] += BT(r) * vv;
+                        const int R = R0 + r;
+                        if (R == 0 || R == h - 1) {
+                            pR[q_of(r)] = sr[r];
+                            pV2[q_of(r)] = vv;
+                        }
                     }
-                }
-                block_reduce2<1, 0>(a, red);
-                if (tid == 0) S.part[((long long)set * G + g) * NPART] = a[0];
-                PMARK(1);
-            } else if (!epi_done) {
-                double a[3] = {0.0, 0.0, 0.0};
-                #pragma unroll
-                for (int r = 0; r < RMAX; ++r) {
-                    if (r >= hs) continue;
-                    double dx = X(r);
-                    if (pending) dx += alpha * pp[r] + omega * sr[r];
-                    const long long q = q_of(r);
-                    if (S.mode == 1) S.xptr[me][q] = dx;
-                    else {
-                        pX[q] = dx;
-                        Unew[q] = u_s[uidx(r)] + dx;
+                } else if (do_epi) {
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) {
+                        if (r >= hs) continue;
+                        double dx = X(r);
+                        if (pending) dx += alpha * pp[r] + omega * sr[r];
+                        const long long q = q_of(r);
+                        if (S.mode == 1) S.xptr[me][q] = dx;
+                        else {
+                            pX[q] = dx;
+                            Unew[q] = u_s[uidx(r)] + dx;
+                        }
+                        a[1] += dx * dx;
+                        a[2] = fmax(a[2], fabs(dx));
+                        if (!isfinite(dx)) a[3] = 1.0;
                     }
-                    a[0] += dx * dx;
-                    a[1] = fmax(a[1], fabs(dx));
-                    if (!isfinite(dx)) a[2] = 1.0;
+                    pending = false;
                 }
-                block_reduce2<1, 2>(a, red);
+                block_reduce2<2, 2>(a, red);
                 if (tid == 0) {
-                    hp[g * 4 + 2] = a[0];
-                    hp[g * 4 + 3] = a[1];
-                    if (a[2] != 0.0) atomicOr(&S.bs->err, 1u);
+                    if (do_p1) S.part[((long long)set * G + g) * NPART] = a[0];
+                    if (do_epi) {
+                        hp[g * 4 + 2] = a[1];
+                        hp[g * 4 + 3] = a[2];
+                        if (a[3] != 0.0) atomicOr(&S.bs->err, 1u);
+                    }
                 }
-                epi_done = true;
-                pending = false;
-                PMARK(3);
-            }
-            const bool any = bar_sync(S.bs, G, ep, !conv, hi);
-            PMARK(4);
-            if (!any) { set ^= 1; break; }
-            double r0v = 0.0;
-            if (!conv) {
-                double o[1];
-                pair_reduce2<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
-                r0v = o[0];
-            }
-            PMARK(5);
-            set ^= 1;
-            if (!conv) {
-                if (r0v == 0.0 || !isfinite(r0v)) {
-                    if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
-                    conv = true;
-                } else {
-                    alpha = rho / r0v;
+                if (do_epi) epi_done = true;
+                PMARK(1);
+                const bool any = bar_sync(S.bs, G, ep, !conv, hi);
+                PMARK(4);
+                if (!any) { set ^= 1; break; }
+                double o1[1];
+                pair_reduce2<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o1, s_red);
+                const double r0v = o1[0];
+                PMARK(5);
+                set ^= 1;
+                if (!conv) {
+                    if (r0v == 0.0 || !isfinite(r0v)) {
+                        if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                        conv = true;
+                    } else {
+                        alpha = rho / r0v;
+                    }
                 }
             }
-            }   // !fused_first
             fused_first = false;
             // ================= phase 2: s = r - alpha v, t = A s ====================================
-            if (!conv) {
+            {
                 double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // (t,s) (t,t) (b~,s) (b~,t) (s,s)
-                double hS[2] = {0.0, 0.0}, hN[2] = {0.0, 0.0};
-                if (hs > 0 && own_top && top_valid) {
-                    const long long q = (long long)top_row * nxu + col;
-                    hS[0] = __ldcg(pR + q); hS[1] = __ldcg(pV2 + q);
-                }
-                if (hs > 0 && own_bot && bot_valid) {
-                    const long long q = (long long)bot_row * nxu + col;
-                    hN[0] = __ldcg(pR + q); hN[1] = __ldcg(pV2 + q);
-                }
-                #pragma unroll
-                for (int r = 0; r < RMAX; ++r) {
-                    if (r >= hs) continue;
-                    const double s = sr[r] - alpha * v_s[r * BLOCK3 + tid];
-                    sr[r] = s;
-                    put_op(r, s);
-                }
-                const double haloS = hS[0] - alpha * hS[1], haloN = hN[0] - alpha * hN[1];
-                __syncthreads();
-                #pragma unroll
-                for (int r = 0; r < RMAX; ++r) {
-                    if (r >= hs) continue;
-                    const int si = sidx(r);
-                    const Off o = coef(r);
-                    const double s = sr[r];
-                    const double t = s + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(sr, r, haloN) +
-                                                    o.s * opS(sr, r, haloS));
-                    t_s[r * BLOCK3 + tid] = t;
-                    const double b0 = BT(r);
-                    a[0] += t * s; a[1] += t * t; a[2] += b0 * s; a[3] += b0 * t; a[4] += s * s;
-                    const int R = R0 + r;
-                    if (R == 0 || R == h - 1) {
-                        const long long q = q_of(r);
-                        pS[q] = s; pT[q] = t; pP[q] = pp[r]; pV[q] = v_s[r * BLOCK3 + tid];
+                if (!conv) {
+                    double hS[2] = {0.0, 0.0}, hN[2] = {0.0, 0.0};
+                    if (hasS) {
+                        const long long q = (long long)top_row * nxu + col;
+                        hS[0] = __ldcg(pR + q); hS[1] = __ldcg(pV2 + q);
+                    }
+                    if (hasN) {
+                        const long long q = (long long)bot_row * nxu + col;
+                        hN[0] = __ldcg(pR + q); hN[1] = __ldcg(pV2 + q);
+                    }
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) {
+                        if (r >= hs) continue;
+                        const double sv = sr[r] - alpha * v_s[r * BLOCK3 + tid];
+                        sr[r] = sv;
+                        put_op(r, sv);
+                    }
+                    const double haloS = hS[0] - alpha * hS[1], haloN = hN[0] - alpha * hN[1];
+                    __syncthreads();
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) {
+                        if (r >= hs) continue;
+                        const int si = sidx(r);
+                        const Off o = coef(r);
+                        const double sv = sr[r];
+                        const double t = sv + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(sr, r, haloN) +
+                                                         o.s * opS(sr, r, haloS));
+                        t_s[r * BLOCK3 + tid] = t;
+                        const double b0 = BT(r);
+                        a[0] += t * sv; a[1] += t * t; a[2] += b0 * sv; a[3] += b0 * t; a[4] += sv * sv;
+                        const int R = R0 + r;
+                        if (R == 0 || R == h - 1) {
+                            const long long q = q_of(r);
+                            pS[q] = sv; pT[q] = t; pP[q] = pp[r]; pV[q] = v_s[r * BLOCK3 + tid];
+                        }
                     }
                 }
                 block_reduce2<5, 0>(a, red);
-                if (tid == 0) {
+                if (tid == 0 && !conv) {
                     double* pq = S.part + ((long long)set * G + g) * NPART;
                     for (int j = 0; j < 5; ++j) pq[j] = a[j];
                 }
@@ -501,30 +495,32 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             }
             bar_sync(S.bs, G, ep, false, hi);
             PMARK(4);
-            if (!conv) {
+            {
                 double o[5];
                 pair_reduce2<5, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
-                const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];
-                ++it;
-                pending = true;
-                if (tt2 == 0.0) {
-                    omega = 0.0;
-                    conv = true;
-                } else {
-                    omega = ts / tt2;
-                    const double rhon = r0s - omega * r0t;
-                    const double rn2 = fmax(ss - 2.0 * omega * ts + omega * omega * tt2, 0.0);
-                    if (!isfinite(omega) || !isfinite(rn2)) {
-                        if (tid == 0 && c == 0) atomicOr(&S.bs->err, 1u);
-                        conv = true;
-                    } else if (rn2 <= rtol2 * bnorm2 || rn2 <= atol2 || it >= S.lin_max) {
-                        conv = true;
-                    } else if (omega == 0.0 || rhon == 0.0) {
-                        if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                if (!conv) {
+                    const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];
+                    ++it;
+                    pending = true;
+                    if (tt2 == 0.0) {
+                        omega = 0.0;
                         conv = true;
                     } else {
-                        beta = (rhon / rho) * (alpha / omega);
-                        rho = rhon;
+                        omega = ts / tt2;
+                        const double rhon = r0s - omega * r0t;
+                        const double rn2 = fmax(ss - 2.0 * omega * ts + omega * omega * tt2, 0.0);
+                        if (!isfinite(omega) || !isfinite(rn2)) {
+                            if (tid == 0 && c == 0) atomicOr(&S.bs->err, 1u);
+                            conv = true;
+                        } else if (rn2 <= rtol2 * bnorm2 || rn2 <= atol2 || it >= S.lin_max) {
+                            conv = true;
+                        } else if (omega == 0.0 || rhon == 0.0) {
+                            if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                            conv = true;
+                        } else {
+                            beta = (rhon / rho) * (alpha / omega);
+                            rho = rhon;
+                        }
                     }
                 }
             }

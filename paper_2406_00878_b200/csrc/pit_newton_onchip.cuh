@@ -71,7 +71,7 @@ __device__ __forceinline__ void pair_reduce2(const double* part, int stride, int
         for (int i = 0; i < N; ++i) sm[i * GMAX2 + threadIdx.x] = __ldcg(pg + i);
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
+    if ((threadIdx.x >> 5) == 0) {                      // warp 0 (a warp-uniform condition)
         double a[N];
         #pragma unroll
         for (int i = 0; i < N; ++i) a[i] = 0.0;
