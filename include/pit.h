@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define PIT_ABI_VERSION 1
+#define PIT_ABI_VERSION 2
 
 typedef enum {
     PIT_OK = 0,           /* converged: max|dU_k| <= newton_tol */
@@ -72,7 +72,7 @@ typedef struct {
     double  x0, x1, y0, y1;/* domain [x0,x1] x [y0,y1]; h_x = (x1-x0)/nx */
     double  dt;            /* uniform time step tau > 0 */
     double  m0, m2;        /* mu(u) = m0 + m2 u^2, m0, m2 >= 0 (paper heat: 0, mu0; Burgers: mu0, 0) */
-    double  newton_tol;    /* stop on max|dU_k| <= newton_tol (> 0; BASELINE: 1e-12) */
+    double  newton_tol;    /* stop on ||dU_k|| <= newton_tol (> 0; BASELINE: 1e-12), norm chosen by stop_norm */
     int32_t newton_max;    /* max Newton iterations (1..256) */
     double  lin_rtol;      /* per-level solve: ||b~ - A~ x||_2 <= lin_rtol ||b~||_2 (A~ = diag-scaled A_n);
                               0 = default 1e-10 */
@@ -86,6 +86,15 @@ typedef struct {
                               1 = global-state engine (any size), 2 = strip on-chip engine, 3 = column-blocked
                               on-chip engine (nx = 256 or 512 unknowns per row); 2/3: PIT_EINVAL if they do
                               not fit the registers + shared memory of one SM per CTA */
+    int32_t guess_cf;      /* initial Newton iterate when the caller passes no guess:
+                              0 = u^0 at every level; c_f >= 2 = the paper's coarse-grid guess: sequential-
+                              equivalent BDF1 solve on the grid coarsened by c_f in x, y and t (the same
+                              all-at-once solver, on the device), then cubic-spline interpolation along x, y
+                              (periodic splines on periodic grids, not-a-knot otherwise) and t (not-a-knot,
+                              u^0 as the t = 0 knot).  c_f must divide nx, ny and nt; coarse grid >= 2
+                              (Dirichlet) / >= 3 (periodic) intervals.  Paper: 4 (heat), 3 (Burgers) */
+    int32_t stop_norm;     /* 0 = max|dU_k| (default); 1 = the paper's L2 update norm
+                              sqrt(sum (dU_k)^2 / (nt ns)) */
 } pit_config;
 
 typedef struct pit_handle pit_handle;
@@ -142,10 +151,15 @@ int pit_product_window_device(pit_handle* h, int32_t s0, int32_t L, const double
                               const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
                               int32_t* d_info, void* cuda_stream);
 
+/* The initial Newton iterate on its own: with guess_cf >= 2 the coarse-grid solve + spline
+ * interpolation described at pit_config.guess_cf, else u^0 at every level; written to d_U0 [nt][ns] (device).
+ * d_u0 [ns], d_bc as in pit_solve_device.  Asynchronous on cuda_stream. */
+int pit_initial_guess_device(pit_handle* h, const double* d_u0, const double* d_bc, double* d_U0, void* cuda_stream);
+
 /* Number of unknowns per level and device bytes the handle holds. */
 int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
 
-/* Pipeline statistics of the last solve (synchronizes with it):
+/* Pipeline statistics of the last solve (synchronizes with it; n >= 17 + 256 + 7 for every field):
  * out[0] = wavefront steps, out[1] = total BiCGSTAB iterations summed over steps (max per step),
  * out[2] = pipeline depth used, out[3] = grid CTAs, out[4] = kernel launches of the last solve,
  * out[5] = device time of the persistent Newton kernel of the last solve [ns] (CUDA events on the
@@ -155,7 +169,9 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * environment variable PIT_TRACE was set at pit_create (zeros otherwise), out[15] = 1 if the last solve
  * inverted Eq. (6) with the (b2) product form (inverse_mode PRODUCT_WINDOW, or AUTO with the whole horizon
  * inside the Section 7 gate), 0 for the on-device level recurrence, out[16] = BiCGSTAB iterations summed
- * over all (level, iteration) pairs (on-chip engine), out[17 + k] = those of Newton iteration k. */
+ * over all (level, iteration) pairs (on-chip engine), out[17 + k] = those of Newton iteration k,
+ * out[273..278] = prologue sub-categories of the cycle accounting, out[279] = device time of the coarse-grid
+ * initial guess (coarse solve + interpolation) [ns], 0 without it. */
 int pit_stats(pit_handle* h, int64_t* out, int32_t n);
 
 const char* pit_strerror(int code);

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "pit_kernels.cu"
+#include "pit_guess.cuh"
 
 using namespace pit;
 
@@ -47,8 +48,16 @@ struct pit_handle {
     double* d_small = nullptr;    // [2 * 1024] scratch for kernel (a) partials + norms
     long long bytes = 0;
     long long launches = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // k_init start/end, k_newton start/end
-    bool timed = false;
+    cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // k_init, k_newton, guess start/end
+    bool timed = false, guess_timed = false;
+    // coarse-grid initial guess (guess_cf >= 2): nested handle on the coarsened problem
+    pit_handle* coarse = nullptr;
+    GuessParams gp;
+    double* c_u0 = nullptr;       // [nsc]
+    double* c_ring = nullptr;     // [ntc][ring_len_c] (Dirichlet)
+    double* c_U = nullptr;        // [ntc][nsc] coarse solution
+    double* c_fac = nullptr;      // [2][Kmax] spline factors
+    int* c_info = nullptr;        // [2]
     char err[512] = {0};
 };
 
@@ -116,6 +125,13 @@ static int validate(const pit_config* c, char* why, size_t n) {
     if (c->inverse_mode < 0 || c->inverse_mode > 2) { snprintf(why, n, "inverse_mode %d", c->inverse_mode); return PIT_EINVAL; }
     if (c->pipeline_depth < 0 || c->pipeline_depth > MAXD) { snprintf(why, n, "pipeline_depth must be in 0..%d", MAXD); return PIT_EINVAL; }
     if (c->window < 0) { snprintf(why, n, "window < 0"); return PIT_EINVAL; }
+    if (c->stop_norm < 0 || c->stop_norm > 1) { snprintf(why, n, "stop_norm %d", c->stop_norm); return PIT_EINVAL; }
+    if (c->guess_cf == 1 || c->guess_cf < 0) { snprintf(why, n, "guess_cf must be 0 or >= 2"); return PIT_EINVAL; }
+    if (c->guess_cf >= 2) {
+        const int f = c->guess_cf;
+        if (c->nx % f || c->ny % f || c->nt % f) { snprintf(why, n, "guess_cf %d must divide nx, ny and nt", f); return PIT_EINVAL; }
+        if (c->nx / f < nmin || c->ny / f < nmin) { snprintf(why, n, "coarse grid below %d intervals", nmin); return PIT_EINVAL; }
+    }
     return PIT_OK;
 }
 
@@ -125,6 +141,9 @@ static void free_all(pit_handle* h) {
     cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
     cudaFree(h->d_small); cudaFree(h->bs); cudaFree(h->trace);
     cudaFree(h->pf_Y); cudaFree(h->pf_R); cudaFree(h->pf_dU); cudaFree(h->pf_part);
+    cudaFree(h->c_u0); cudaFree(h->c_ring); cudaFree(h->c_U); cudaFree(h->c_fac); cudaFree(h->c_info);
+    h->c_u0 = h->c_ring = h->c_U = h->c_fac = nullptr; h->c_info = nullptr;
+    if (h->coarse) { pit_destroy(h->coarse); h->coarse = nullptr; }
     h->bs = nullptr; h->trace = nullptr; h->pf_Y = h->pf_R = h->pf_dU = h->pf_part = nullptr;
     h->U = h->slots = h->part = h->hpart = h->hist = h->d_u0 = h->d_bc = h->d_small = nullptr;
     h->bar = nullptr; h->info = nullptr; h->stats = nullptr;
@@ -167,6 +186,36 @@ static const void* col_fn(int rmax, bool trace, int law) {
 static const void* onchip_fn(int ppt, bool trace, int law) {
     if (law == 1) return trace ? onchip_fn_t<true, 1>(ppt) : onchip_fn_t<false, 1>(ppt);
     return trace ? onchip_fn_t<true, 0>(ppt) : onchip_fn_t<false, 0>(ppt);
+}
+
+// The c_f-coarsened problem of the initial guess: N_x / c_f, N_y / c_f intervals, N_t / c_f levels
+// of step c_f dt, same law, domain and solver settings.  "Solving Eq. (FDS) sequentially": the nested handle is
+// a ONE-level problem; build_guess marches it level by level (u^0 of level m = the converged level m-1), so its
+// Newton iteration at each level is exactly the sequential method's (same engines, on the device).
+static int create_coarse(pit_handle* h) {
+    const pit_config& c = h->cfg;
+    const int f = c.guess_cf;
+    pit_config cc = c;
+    cc.nx = c.nx / f; cc.ny = c.ny / f; cc.nt = 1; cc.dt = c.dt * f;
+    cc.guess_cf = 0; cc.pipeline_depth = 0; cc.engine = 0; cc.window = 0; cc.stop_norm = 0;
+    cc.inverse_mode = PIT_INV_RECURRENCE;
+    int rc = pit_create(&cc, &h->coarse);
+    if (rc != PIT_OK) return set_err(h, rc, "coarse-grid handle: %s", pit_strerror(rc));
+    GuessParams& g = h->gp;
+    std::memset(&g, 0, sizeof(g));
+    const Prob& P = h->P;
+    const Prob& Q = h->coarse->P;
+    g.cf = f; g.bc = P.bc;
+    g.nx = P.nx; g.ny = P.ny; g.nt = P.nt; g.nxu = P.nxu; g.nyu = P.nyu; g.ns = P.ns;
+    g.nxc = Q.nx; g.nyc = Q.ny; g.ntc = P.nt / f; g.nxuc = Q.nxu; g.nyuc = Q.nyu; g.nsc = Q.ns; g.ring_len_c = Q.ring_len;
+    const int kmax = std::max(std::max(Q.nx, Q.ny) + 1, g.ntc + 1);
+    if ((rc = dalloc(h, &h->c_u0, (size_t)Q.ns)) ||
+        (rc = dalloc(h, &h->c_ring, (size_t)(P.bc == PIT_DIRICHLET ? (long long)g.ntc * Q.ring_len : 1))) ||
+        (rc = dalloc(h, &h->c_U, (size_t)(Q.ns * g.ntc))) ||
+        (rc = dalloc(h, &h->c_fac, (size_t)(2 * kmax))) ||
+        (rc = dalloc(h, &h->c_info, 2)))
+        return rc;
+    return PIT_OK;
 }
 
 int pit_create(const pit_config* cfg, pit_handle** out) {
@@ -319,6 +368,11 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         delete h;
         return PIT_ECUDA;
     }
+    if (c.guess_cf >= 2 && (rc = create_coarse(h)) != PIT_OK) {
+        free_all(h);
+        delete h;
+        return rc;
+    }
     *out = h;
     return PIT_OK;
 }
@@ -368,6 +422,7 @@ static SolveParams base_params(pit_handle* h) {
     S.newton_max = h->cfg.newton_max;
     S.lin_max = h->cfg.lin_max;
     S.stats = h->stats;
+    S.stop_norm = h->cfg.stop_norm;
     return S;
 }
 
@@ -382,12 +437,11 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
         if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 13 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
         CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
-        if (h->engine == 3)
-            CUDA_TRY(h, cudaLaunchCooperativeKernel(col_fn(h->ppt, h->trace != nullptr, h->law), dim3(h->G), dim3(BLOCK3), args,
-                                                    h->smem2, st));
-        else
-            CUDA_TRY(h, cudaLaunchCooperativeKernel(onchip_fn(h->ppt, h->trace != nullptr, h->law), dim3(h->G), dim3(BLOCK2),
-                                                    args, h->smem2, st));
+        // the dynamic shared-memory limit is a per-function attribute shared by every handle of the process
+        // (e.g. the nested coarse-grid handle): set it for this launch
+        const void* fn = h->engine == 3 ? col_fn(h->ppt, h->trace != nullptr, h->law) : onchip_fn(h->ppt, h->trace != nullptr, h->law);
+        CUDA_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem2));
+        CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->G), dim3(h->engine == 3 ? BLOCK3 : BLOCK2), args, h->smem2, st));
     } else {
         CUDA_TRY(h, cudaMemsetAsync(h->bar, 0, sizeof(GridBar), st));
         CUDA_TRY(h, cudaLaunchCooperativeKernel((void*)k_newton, dim3(h->G), dim3(BLOCK), args, 0, st));
@@ -470,9 +524,10 @@ static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, 
         hist[4 * k + 2] = std::sqrt(s2 / (double)N); hist[4 * k + 3] = mx;
         kdone = k + 1;
         if (bad != 0.0) { status = PIT_EBREAKDOWN; break; }
-        if (mx <= h->cfg.newton_tol) { status = PIT_OK; break; }
-        if (k >= 1 && mx > 0.5 * prevmax && mx <= 1e3 * h->cfg.newton_tol) { status = PIT_OK_FLOOR; break; }
-        prevmax = mx;
+        const double dn = h->cfg.stop_norm ? hist[4 * k + 2] : mx;
+        if (dn <= h->cfg.newton_tol) { status = PIT_OK; break; }
+        if (k >= 1 && dn > 0.5 * prevmax && dn <= 1e3 * h->cfg.newton_tol) { status = PIT_OK_FLOOR; break; }
+        prevmax = dn;
     }
     if (d_u_out) CUDA_TRY(h, cudaMemcpyAsync(d_u_out, U, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
     if (d_hist) CUDA_TRY(h, cudaMemcpyAsync(d_hist, hist.data(), sizeof(double) * 4 * kmax, cudaMemcpyHostToDevice, st));
@@ -494,14 +549,73 @@ static bool want_product(pit_handle* h, const double* d_bc, cudaStream_t st) {
     return chain_bound(an.data(), h->P.nt) <= PIT_GATE;
 }
 
+// The paper's initial iterate (pit_guess.cuh), written into iterate buffer 0.  Iterate
+// buffers 1 and 2 are free before the Newton launch and serve as the interpolation scratch (B >= 3).
+static int build_guess(pit_handle* h, const double* d_u0, const double* d_bc, cudaStream_t st) {
+    GuessParams g = h->gp;
+    const Prob& P = h->P;
+    const long long N = P.ns * P.nt;
+    g.u0f = d_u0;
+    g.cring = (P.bc == PIT_DIRICHLET && d_bc) ? h->c_ring : nullptr;
+    g.cU = h->c_U;
+    g.fac = h->c_fac;
+    g.Tx = h->U + N;
+    g.Ty = g.Tx + (long long)g.ntc * (g.bc == 1 ? g.nyc : g.nyc + 1) * g.nxu;
+    g.tmp = h->U + 2 * N;
+    g.U0 = h->U;
+    CUDA_TRY(h, cudaEventRecord(h->ev[4], st));
+    k_restrict_u0<<<grid_for(g.nsc, h->sms), BLOCK, 0, st>>>(g, h->c_u0);
+    CUDA_TRY(h, cudaGetLastError());
+    int nl = 1;
+    if (g.cring) {
+        k_restrict_ring<<<grid_for((long long)g.ntc * g.ring_len_c, h->sms), BLOCK, 0, st>>>(g, d_bc, h->c_ring);
+        CUDA_TRY(h, cudaGetLastError());
+        ++nl;
+    }
+    long long cl = 0;
+    for (int m = 1; m <= g.ntc; ++m) {                 // sequential BDF1 on the coarse grid
+        const double* um1 = m == 1 ? h->c_u0 : h->c_U + (long long)(m - 2) * g.nsc;
+        const double* rg = g.cring ? h->c_ring + (long long)(m - 1) * g.ring_len_c : nullptr;
+        int rc = pit_solve_device(h->coarse, um1, rg, nullptr, h->c_U + (long long)(m - 1) * g.nsc, nullptr, h->c_info, st);
+        if (rc != PIT_OK) return set_err(h, rc, "coarse-grid solve, level %d: %s", m, pit_last_error(h->coarse));
+        cl += h->coarse->launches;
+    }
+    const int NR = g.bc == 1 ? g.nyc : g.nyc + 1, NC = g.bc == 1 ? g.nxc : g.nxc + 1;
+    const long long lines[3] = {(long long)g.ntc * NR, (long long)g.ntc * g.nxu, g.ns};
+    const int K[3] = {NC, NR, g.ntc + 1};
+    for (int pass = 0; pass < 3; ++pass) {
+        const int per = pass < 2 && g.bc == 1;
+        k_spline_setup<<<1, 1, 0, st>>>(K[pass], per, h->c_fac);
+        CUDA_TRY(h, cudaGetLastError());
+        const int gr = (int)std::max<long long>(1, std::min<long long>((lines[pass] + 255) / 256, (long long)h->sms * 16));
+        if (pass == 0) k_spline<0><<<gr, 256, 0, st>>>(g);
+        else if (pass == 1) k_spline<1><<<gr, 256, 0, st>>>(g);
+        else k_spline<2><<<gr, 256, 0, st>>>(g);
+        CUDA_TRY(h, cudaGetLastError());
+        nl += 2;
+    }
+    CUDA_TRY(h, cudaEventRecord(h->ev[5], st));
+    h->launches += nl + cl;
+    h->guess_timed = true;
+    return PIT_OK;
+}
+
 int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, const double* d_guess, double* d_u_out,
                      double* d_hist, int32_t* d_info, void* cuda_stream) {
     if (!h || !d_u0 || !d_u_out) return set_err(h, PIT_EINVAL, "null argument");
     CUDA_TRY(h, cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)cuda_stream;
     h->launches = 0;
-    int rc = launch_init(h, d_u0, d_guess, st);
-    if (rc != PIT_OK) return rc;
+    h->guess_timed = false;
+    int rc;
+    if (!d_guess && h->coarse) {
+        if ((rc = build_guess(h, d_u0, d_bc, st)) != PIT_OK) return rc;
+        CUDA_TRY(h, cudaEventRecord(h->ev[0], st));       // U_0 is already in place: no init kernel
+        CUDA_TRY(h, cudaEventRecord(h->ev[1], st));
+        h->timed = true;
+    } else if ((rc = launch_init(h, d_u0, d_guess, st)) != PIT_OK) {
+        return rc;
+    }
     if (d_hist) CUDA_TRY(h, cudaMemsetAsync(d_hist, 0, sizeof(double) * 4 * h->cfg.newton_max, st));
     h->product_used = false;
     if (want_product(h, d_bc, st)) return solve_product(h, d_u0, d_bc, d_u_out, d_hist, (int*)d_info, st);
@@ -513,6 +627,21 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
     S.info = d_info ? (int*)d_info : h->info;
     S.mode = 0;
     return launch_newton(h, S, st);
+}
+
+int pit_initial_guess_device(pit_handle* h, const double* d_u0, const double* d_bc, double* d_U0, void* cuda_stream) {
+    if (!h || !d_u0 || !d_U0) return set_err(h, PIT_EINVAL, "null argument");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    h->launches = 0;
+    int rc;
+    if (h->coarse) {
+        if ((rc = build_guess(h, d_u0, d_bc, st)) != PIT_OK) return rc;
+    } else if ((rc = launch_init(h, d_u0, nullptr, st)) != PIT_OK) {
+        return rc;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(d_U0, h->U, sizeof(double) * h->P.ns * h->P.nt, cudaMemcpyDeviceToDevice, st));
+    return PIT_OK;
 }
 
 int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* guess, double* u_out, double* hist,
@@ -729,6 +858,11 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];
     for (int i = 17; i < n && i < 17 + MAXK; ++i) out[i] = s[8 + (i - 17)];
     for (int i = 17 + MAXK; i < n && i < 17 + MAXK + 6; ++i) out[i] = (long long)tr[7 + (i - 17 - MAXK)];
+    if (n > 17 + MAXK + 6) {
+        float t_guess = 0.f;
+        if (h->guess_timed) CUDA_TRY(h, cudaEventElapsedTime(&t_guess, h->ev[4], h->ev[5]));
+        out[17 + MAXK + 6] = (long long)(t_guess * 1e6);
+    }
     return PIT_OK;
 }
 

@@ -738,12 +738,12 @@ __global__ void __launch_bounds__(BLOCK2, 1) k_newton_onchip(SolveParams S) {
             if (S.mode == 0 && na == P.nt) {
                 last_done = k;
                 const double Ntot = (double)ns * (double)P.nt;
-                const double dmax = hacc[sa][3];
+                const double dmax = S.stop_norm ? sqrt(hacc[sa][2] / Ntot) : hacc[sa][3];   // stop norm
                 if (g == 0 && tid == 0) {
                     S.hist[4 * k + 0] = sqrt(hacc[sa][0] / Ntot);
                     S.hist[4 * k + 1] = hacc[sa][1];
                     S.hist[4 * k + 2] = sqrt(hacc[sa][2] / Ntot);
-                    S.hist[4 * k + 3] = dmax;
+                    S.hist[4 * k + 3] = hacc[sa][3];
                 }
                 if (dmax <= S.newton_tol) { stop_status = 0; stop_k = k; }
                 else if (k >= 1 && dmax > 0.5 * prevmax_s && dmax <= 1e3 * S.newton_tol) { stop_status = 1; stop_k = k; }

@@ -16,7 +16,7 @@ from . import workloads as W
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpit.so")
 
-PIT_ABI_VERSION = 1
+PIT_ABI_VERSION = 2
 PIT_OK, PIT_OK_FLOOR, PIT_EINVAL, PIT_ENOMEM, PIT_ECUDA, PIT_ENOCONV, PIT_EBREAKDOWN, PIT_ECOND = 0, 1, -1, -2, -3, -4, -5, -6
 PIT_HEAT, PIT_BURGERS = 0, 1
 PIT_DIRICHLET, PIT_PERIODIC = 0, 1
@@ -24,7 +24,7 @@ PIT_INV_AUTO, PIT_INV_RECURRENCE, PIT_INV_PRODUCT_WINDOW = 0, 1, 2
 
 # every symbol include/pit.h declares (tests check the library exports all of them)
 EXPORTS = ["pit_config_init", "pit_create", "pit_destroy", "pit_solve", "pit_solve_device", "pit_residual_device",
-           "pit_level_solve_device", "pit_product_window_device", "pit_sizes", "pit_stats", "pit_strerror",
+           "pit_level_solve_device", "pit_product_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_strerror",
            "pit_last_error", "pit_abi_version"]
 
 
@@ -35,7 +35,7 @@ class PitConfig(C.Structure):
                 ("newton_tol", C.c_double), ("newton_max", C.c_int32), ("lin_rtol", C.c_double),
                 ("lin_atol", C.c_double), ("lin_max", C.c_int32), ("inverse_mode", C.c_int32),
                 ("window", C.c_int32), ("pipeline_depth", C.c_int32), ("device", C.c_int32),
-                ("engine", C.c_int32)]
+                ("engine", C.c_int32), ("guess_cf", C.c_int32), ("stop_norm", C.c_int32)]
 
 
 class PitError(RuntimeError):
@@ -65,6 +65,7 @@ def lib():
         L.pit_level_solve_device.restype = C.c_int
         L.pit_product_window_device.argtypes = [hp, C.c_int32, C.c_int32, dp, dp, dp, dp, dp, dp, i32p, vp]
         L.pit_product_window_device.restype = C.c_int
+        L.pit_initial_guess_device.argtypes = [hp, dp, dp, dp, vp]; L.pit_initial_guess_device.restype = C.c_int
         L.pit_sizes.argtypes = [hp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]; L.pit_sizes.restype = C.c_int
         L.pit_stats.argtypes = [hp, C.POINTER(C.c_int64), C.c_int32]; L.pit_stats.restype = C.c_int
         L.pit_strerror.argtypes = [C.c_int]; L.pit_strerror.restype = C.c_char_p
@@ -148,6 +149,9 @@ class Solver:
         return self._check(lib().pit_residual_device(self.h, _ptr(d_U), _ptr(d_u0), _ptr(d_ring), _ptr(d_R),
                                                      _ptr(d_diag), _ptr(d_norms), _stream(stream)))
 
+    def initial_guess_device(self, d_u0, d_ring, d_U0, stream=None) -> int:
+        return self._check(lib().pit_initial_guess_device(self.h, _ptr(d_u0), _ptr(d_ring), _ptr(d_U0), _stream(stream)))
+
     def level_solve_device(self, level, d_U, d_ring, d_b, d_x, d_info, stream=None) -> int:
         return self._check(lib().pit_level_solve_device(self.h, level, _ptr(d_U), _ptr(d_ring), _ptr(d_b),
                                                         _ptr(d_x), _ptr(d_info), _stream(stream)))
@@ -158,12 +162,13 @@ class Solver:
                                                            _stream(stream)))
 
     def stats(self):
-        out = (C.c_int64 * (17 + 256 + 6))()
-        self._check(lib().pit_stats(self.h, out, 17 + 256 + 6))
+        out = (C.c_int64 * (17 + 256 + 7))()
+        self._check(lib().pit_stats(self.h, out, 17 + 256 + 7))
         d = {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
              "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6, "engine": out[7],
              "product_form": bool(out[15]), "pair_iterations": out[16],
-             "iterations_per_newton_k": [out[17 + k] for k in range(256) if out[17 + k]]}
+             "iterations_per_newton_k": [out[17 + k] for k in range(256) if out[17 + k]],
+             "guess_ms": out[279] * 1e-6}
         if any(out[8:15]):
             names = ["prologue", "phase1", "phase2", "epilogue", "barrier", "reduce", "step_tail"]
             d["trace_cycles_per_cta"] = {k: out[8 + i] / max(1, out[3]) for i, k in enumerate(names)}

@@ -42,8 +42,8 @@ def test_config_struct_layout_matches_header(built):
     # offsets the C compiler sees: pit_config_init writes abi_version/newton_tol/newton_max at their C offsets
     c = pit.PitConfig()
     built.pit_config_init(C.byref(c))
-    assert c.abi_version == 1 and c.newton_tol == 1e-12 and c.newton_max == 30 and c.x1 == 1.0 and c.y1 == 1.0
-    assert c.pde == 0 and c.device == 0 and c.pipeline_depth == 0
+    assert c.abi_version == pit.PIT_ABI_VERSION == 2 and c.newton_tol == 1e-12 and c.newton_max == 30 and c.x1 == 1.0 and c.y1 == 1.0
+    assert c.pde == 0 and c.device == 0 and c.pipeline_depth == 0 and c.guess_cf == 0 and c.stop_norm == 0
 
 
 def test_strerror(built):
@@ -52,7 +52,8 @@ def test_strerror(built):
 
 
 @pytest.mark.parametrize("field,value", [("abi_version", 7), ("nx", 1), ("nt", 0), ("dt", 0.0), ("m0", -1.0),
-                                         ("newton_max", 0), ("pipeline_depth", 99), ("bc", 5)])
+                                         ("newton_max", 0), ("pipeline_depth", 99), ("bc", 5),
+                                         ("guess_cf", 1), ("guess_cf", 5), ("guess_cf", -2), ("stop_norm", 2)])
 def test_invalid_config_rejected_before_touching_the_gpu(built, field, value):
     c = pit.make_config(W.config(1))
     setattr(c, field, value)
