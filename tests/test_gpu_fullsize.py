@@ -44,3 +44,28 @@ def test_fullsize_config(c):
         mass0 = p.u0.sum()
         drift = np.abs(U.sum(axis=1) - mass0).max()
         assert drift <= 1e-12 * p.ns * max(1.0, np.abs(p.u0).max()), drift
+
+
+def test_fullsize_c5_coarse_guess():
+    """N1 at BASELINE size: the GPU's coarse-grid guess for c5 (c_f = 4: 128^2 x 256 coarse levels) against
+    the oracle's (sequential coarse solve + numpy splines), then the solve from it against the u^0 solve."""
+    from oracle import coarse_guess as CG
+    from gpu_util import dev, normwise_rel, torch_cuda
+    torch = torch_cuda()
+    p = W.config(5)
+    s = pit.Solver(p, guess_cf=4)
+    try:
+        d_U0 = torch.empty((p.nt, p.ns), dtype=torch.float64, device="cuda")
+        s.initial_guess_device(dev(p.u0), None, d_U0)
+        torch.cuda.synchronize()
+        got = d_U0.cpu().numpy()
+        del d_U0
+    finally:
+        s.close()
+    ref = CG.coarse_guess(p, 4)
+    assert normwise_rel(got, ref) <= 1e-9, normwise_rel(got, ref)
+    del got, ref
+    U, hist, nit, st, stats = gpu_solve(p, guess_cf=4)
+    assert st in (pit.PIT_OK, pit.PIT_OK_FLOOR) and nit <= 5
+    seq = O.solve_sequential(p, levels=PREFIX[5])
+    assert np.abs(U[:PREFIX[5]] - seq.U).max() / np.abs(seq.U).max() <= 1e-10
