@@ -396,12 +396,37 @@ static int grid_for(long long n, int sms) {
     return (int)std::max<long long>(1, std::min<long long>(g, (long long)sms * 8));
 }
 
-static void launch_resjac(pit_handle* h, int grid, cudaStream_t st, const double* U, const double* u0, const double* ring,
-                          double* R, double* diag, double* part) {
-    if (h->P.pde == PIT_BURGERS && h->P.m2 == 0.0)
-        k_resjac<1><<<grid, BLOCK, 0, st>>>(h->P, U, u0, ring, R, diag, part);
+// Kernel (a): the TMA-staged k_resjac_bulk when rows are 16-byte multiples and the level bases are 16-byte
+// aligned, else k_resjac.  Returns the number of CTAs whose partial norms are in `part` (<= 1024).
+static int launch_resjac(pit_handle* h, int grid, cudaStream_t st, const double* U, const double* u0, const double* ring,
+                         double* R, double* diag, double* part) {
+    const Prob& P = h->P;
+    const bool law1 = P.pde == PIT_BURGERS && P.m2 == 0.0;
+    const bool aligned = (P.nxu % 2 == 0) && ((uintptr_t)U % 16 == 0) && ((uintptr_t)u0 % 16 == 0) && !getenv("PIT_RESJAC_V1");
+    if (aligned) {
+        const int rowd = P.nxu;
+        // two stages filling the shared memory: the per-tile cost (halo rows, barrier round trips) amortised
+        // over the largest tile (c5: 13 rows of 512, 2 x 112 KB)
+        int NS = 2;
+        int RT = std::max(1, std::min(P.nyu, ((224 * 1024) / (NS * rowd * 8) - 2) / 2));
+        if (getenv("PIT_RESJAC_RT")) RT = std::max(1, atoi(getenv("PIT_RESJAC_RT")));
+        if (getenv("PIT_RESJAC_NS")) NS = std::max(2, std::min(MAXSTAGE, atoi(getenv("PIT_RESJAC_NS"))));
+        const size_t smem = (size_t)NS * (2 * RT + 2) * rowd * sizeof(double);
+        if (smem <= 224 * 1024) {
+            const long long ntiles = (long long)P.nt * ((P.nyu + RT - 1) / RT);
+            const int g = (int)std::max<long long>(1, std::min<long long>(ntiles, std::min(h->sms, 1024)));
+            const void* fn = law1 ? (const void*)k_resjac_bulk<1> : (const void*)k_resjac_bulk<0>;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (law1) k_resjac_bulk<1><<<g, BLOCKA + 32, smem, st>>>(P, U, u0, ring, R, diag, part, RT, NS);
+            else k_resjac_bulk<0><<<g, BLOCKA + 32, smem, st>>>(P, U, u0, ring, R, diag, part, RT, NS);
+            return g;
+        }
+    }
+    if (law1)
+        k_resjac<1><<<grid, BLOCK, 0, st>>>(P, U, u0, ring, R, diag, part);
     else
-        k_resjac<0><<<grid, BLOCK, 0, st>>>(h->P, U, u0, ring, R, diag, part);
+        k_resjac<0><<<grid, BLOCK, 0, st>>>(P, U, u0, ring, R, diag, part);
+    return grid;
 }
 
 static SolveParams base_params(pit_handle* h) {
@@ -490,9 +515,9 @@ static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, 
     double prevmax = INFINITY;
     const int gr = std::min(grid_for(N, h->sms), 1024);
     for (int k = 0; k < kmax; ++k) {
-        launch_resjac(h, gr, st, U, d_u0, ring, h->pf_R, nullptr, h->d_small);
+        const int gpart = launch_resjac(h, gr, st, U, d_u0, ring, h->pf_R, nullptr, h->d_small);
         CUDA_TRY(h, cudaGetLastError());
-        k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, gr, N, h->d_small + 2048);
+        k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, gpart, N, h->d_small + 2048);
         CUDA_TRY(h, cudaGetLastError());
         double rn[2];
         CUDA_TRY(h, cudaMemcpyAsync(rn, h->d_small + 2048, sizeof(rn), cudaMemcpyDeviceToHost, st));
@@ -689,10 +714,10 @@ int pit_residual_device(pit_handle* h, const double* d_U, const double* d_u0, co
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const long long N = h->P.ns * h->P.nt;
     const int grid = std::min(grid_for(N, h->sms), 1024);
-    launch_resjac(h, grid, st, d_U, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_R, d_diag, h->d_small);
+    const int gpart = launch_resjac(h, grid, st, d_U, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_R, d_diag, h->d_small);
     CUDA_TRY(h, cudaGetLastError());
     if (d_norms) {
-        k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, grid, N, d_norms);
+        k_finish_norms<<<1, BLOCK, 0, st>>>(h->d_small, gpart, N, d_norms);
         CUDA_TRY(h, cudaGetLastError());
     }
     return PIT_OK;

@@ -162,6 +162,147 @@ __global__ void __launch_bounds__(BLOCK) k_resjac(Prob P, const double* __restri
     }
 }
 
+// (a) TMA-staged variant: persistent CTAs walk row tiles (level n, rows [j0, j0 + R)) in level-major order.
+// One elected thread stages, per tile, the R + 2 rows of u^n (with the N/S halo rows, wrapped on periodic grids)
+// and the R rows of u^{n-1} into shared memory with 1-D bulk copies (cp.async.bulk, completion on an mbarrier),
+// S tiles ahead; all threads then evaluate the stencil from shared memory and stream R and diag(A_n) out.
+// DRAM: u^n once (u^{n-1} rows were staged nyu / R tiles earlier and hit L2), R and diag written once:
+// 24 B per DOF.  Needs nxu even (16-byte rows) and 16-byte aligned U / u0 (the host checks; else k_resjac).
+constexpr int BLOCKA = 512;
+constexpr int MAXSTAGE = 8;
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(b))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+
+// Warp-specialised: warp NWA (the last) is the producer (one lane issues the bulk copies of tile it + NS once
+// the consumers released the stage on its `empty` mbarrier); warps 0..NWA-1 consume (stencil from shared
+// memory, streaming stores) and release each stage with one arrive per warp.  No CTA-wide barrier per tile.
+constexpr int NWA = BLOCKA / 32;                   // consumer warps
+
+template <int LAW>
+__global__ void __launch_bounds__(BLOCKA + 32, 1) k_resjac_bulk(Prob P, const double* __restrict__ U,
+                                                               const double* __restrict__ u0, const double* __restrict__ ring,
+                                                               double* __restrict__ R, double* __restrict__ diag,
+                                                               double* __restrict__ part, int RT, int NS) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) unsigned long long full[MAXSTAGE], empty[MAXSTAGE];
+    __shared__ double red[NWA * 2];
+    const int nxu = P.nxu, nyu = P.nyu, tid = threadIdx.x, warp = tid >> 5;
+    const bool per = P.bc == 1;
+    const int tpl = (nyu + RT - 1) / RT;                       // tiles per level
+    const long long ntiles = (long long)P.nt * tpl;
+    const int stage = (2 * RT + 2) * nxu;                      // doubles per stage: u^n rows -1..RT, u^{n-1} rows 0..RT-1
+    const unsigned rowb = (unsigned)nxu * 8u;
+    const int nxp = P.nx + 1;
+    const long long stride = gridDim.x;
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWA); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == NWA) {                                         // ---- producer ----
+        if ((tid & 31) == 0) {
+            int it = 0;
+            for (long long t = blockIdx.x; t < ntiles; t += stride, ++it) {
+                const int s = it % NS;
+                if (it >= NS) mbar_wait(&empty[s], (unsigned)(it / NS - 1) & 1u);
+                const int n = (int)(t / tpl), j0 = (int)(t % tpl) * RT;
+                const int rows = min(RT, nyu - j0);
+                double* cur = sm + (long long)s * stage;
+                double* prv = cur + (RT + 2) * nxu;
+                const double* Ul = U + (long long)n * P.ns;
+                const double* Up = n == 0 ? u0 : Ul - P.ns;
+                const bool hasS = per || j0 > 0, hasN = per || j0 + rows < nyu;
+                const unsigned bytes = rowb * (unsigned)(2 * rows + (hasS ? 1 : 0) + (hasN ? 1 : 0));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&full[s], bytes);
+                if (hasS) bulk_g2s(cur, Ul + (long long)(j0 == 0 ? nyu - 1 : j0 - 1) * nxu, rowb, &full[s]);
+                bulk_g2s(cur + nxu, Ul + (long long)j0 * nxu, rowb * rows, &full[s]);
+                if (hasN) bulk_g2s(cur + (rows + 1) * nxu, Ul + (long long)(j0 + rows == nyu ? 0 : j0 + rows) * nxu, rowb, &full[s]);
+                bulk_g2s(prv, Up + (long long)j0 * nxu, rowb * rows, &full[s]);
+            }
+        }
+        return;
+    }
+    double a[2] = {0.0, 0.0};                                  // ---- consumers ----
+    int it = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += stride, ++it) {
+        const int s = it % NS;
+        mbar_wait(&full[s], (unsigned)(it / NS) & 1u);
+        const int n = (int)(t / tpl), j0 = (int)(t % tpl) * RT;
+        const int rows = min(RT, nyu - j0);
+        const double* cur = sm + (long long)s * stage;
+        const double* prv = cur + (RT + 2) * nxu;
+        const double* ringn = ring ? ring + (long long)n * P.ring_len : nullptr;
+        double* Rl = R + (long long)n * P.ns + (long long)j0 * nxu;
+        double* Dl = diag ? diag + (long long)n * P.ns + (long long)j0 * nxu : nullptr;
+        int r = tid / nxu, i = tid - r * nxu;
+        const int di = BLOCKA % nxu, dr = BLOCKA / nxu;
+        for (; r < rows;) {
+            const int e = r * nxu + i, j = j0 + r;
+            const double* row = cur + (r + 1) * nxu;
+            Vals v;
+            v.c = row[i];
+            if (i + 1 < nxu) v.e = row[i + 1];
+            else v.e = per ? row[0] : (ringn ? __ldg(ringn + 2 * nxp + (P.ny - 1) + j) : 0.0);
+            if (i > 0) v.w = row[i - 1];
+            else v.w = per ? row[nxu - 1] : (ringn ? __ldg(ringn + 2 * nxp + j) : 0.0);
+            if (per || j + 1 < nyu) v.n = row[nxu + i];
+            else v.n = ringn ? __ldg(ringn + nxp + i + 1) : 0.0;
+            if (per || j > 0) v.s = row[i - nxu];
+            else v.s = ringn ? __ldg(ringn + i + 1) : 0.0;
+            double G, aC;
+            res_diag<LAW>(P, v, prv[e], G, aC);
+            const double rr = -G;
+            __stcs(Rl + e, rr);
+            if (Dl) __stcs(Dl + e, aC);
+            a[0] += rr * rr;
+            a[1] = fmax(a[1], fabs(rr));
+            i += di; r += dr;
+            if (i >= nxu) { i -= nxu; ++r; }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    }
+    #pragma unroll
+    for (int k = 0; k < 2; ++k)
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, a[k], o);
+            a[k] = k == 0 ? a[k] + y : fmax(a[k], y);
+        }
+    if ((tid & 31) == 0) { red[warp * 2] = a[0]; red[warp * 2 + 1] = a[1]; }
+    asm volatile("bar.sync 1, %0;" ::"r"(BLOCKA) : "memory");   // consumers only (the producer warp has left)
+    if (tid == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int w = 0; w < NWA; ++w) { s0 += red[2 * w]; s1 = fmax(s1, red[2 * w + 1]); }
+        part[2 * blockIdx.x] = s0;
+        part[2 * blockIdx.x + 1] = s1;
+    }
+}
+
 __global__ void k_finish_norms(const double* __restrict__ part, int nparts, long long N, double* __restrict__ norms) {
     __shared__ double red[NWARP * 2];
     double a[2] = {0.0, 0.0};

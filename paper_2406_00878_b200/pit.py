@@ -117,7 +117,10 @@ class Solver:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().pit_destroy(self.h)
+            try:
+                lib().pit_destroy(self.h)
+            except TypeError:          # interpreter shutdown: module globals already torn down
+                pass
             self.h = None
 
     __del__ = close

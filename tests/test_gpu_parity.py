@@ -52,6 +52,36 @@ def test_kernel_a_residual_and_diagonal(idx):
     assert abs(norms[1] - np.abs(Ror).max()) <= 1e-14 * scale
 
 
+@pytest.mark.parametrize("case", ["c3_254_ragged_tiles", "c4_256_periodic", "paper_heat_65_ring", "paper_burgers_33_ring"])
+def test_kernel_a_tma_staged_path(case):
+    """The bulk-copy (TMA) path of kernel (a): even nxu, many row tiles per level, a ragged last tile,
+    wrapped halo rows (periodic) and ring rows (Dirichlet)."""
+    torch = torch_cuda()
+    p = {"c3_254_ragged_tiles": lambda: W.config(3, n=254, nt=3), "c4_256_periodic": lambda: W.config(4, n=256, nt=4),
+         "paper_heat_65_ring": lambda: W.paper_heat(65, nt=3), "paper_burgers_33_ring": lambda: W.paper_burgers(33, nt=2)}[case]()
+    assert p.nxu % 2 == 0
+    rng = np.random.default_rng(7)
+    U = np.tile(p.u0, (p.nt, 1)) + 0.1 * rng.standard_normal((p.nt, p.ns))
+    s = pit.Solver(p)
+    try:
+        dU = dev(U)
+        dR = torch.empty_like(dU)
+        dD = torch.empty_like(dU)
+        dn = torch.zeros(2, dtype=torch.float64, device="cuda")
+        s.residual_device(dU, dev(p.u0), None if p.ring is None else dev(p.ring), dR, dD, dn)
+        torch.cuda.synchronize()
+        R = dR.cpu().numpy()
+    finally:
+        s.close()
+    Ror = O.spacetime_residual(p, U)
+    scale = np.abs(U).max() * (1 + p.dt * (p.m0 + p.m2 * np.abs(U).max() ** 2) * 4 / min(p.hx, p.hy) ** 2)
+    assert np.abs(R - Ror).max() <= 1e-14 * scale
+    diag = np.stack([O.jacobian(p, U[n], n=n + 1)[0] for n in range(p.nt)])
+    assert np.abs(dD.cpu().numpy() - diag).max() <= 1e-14 * np.abs(diag).max()
+    norms = dn.cpu().numpy()
+    assert abs(norms[0] - np.sqrt((Ror ** 2).mean())) <= 1e-12 * norms[0]
+
+
 @pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("idx", range(6))
 def test_stage_c_level_solve_matches_lapack(idx, engine):
