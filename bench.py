@@ -274,10 +274,11 @@ def main():
     t_newton = float(np.median(newton_ms)) * 1e-3
     achieved = BYTES_PER_DOF_IT * p.dof * nit / t_newton / 1e9
     resjac_gbs = RESJAC_BYTES_PER_DOF * p.dof / (resjac_ms * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_a = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(f"c{args.config}", {}).get("k_newton_dram_bytes")
+            tj = json.load(f).get(f"c{args.config}", {})
+            traffic, traffic_a = tj.get("k_newton_dram_bytes"), tj.get("k_resjac_dram_bytes")
     except Exception:
         pass
     line = {
@@ -294,8 +295,9 @@ def main():
                      "algorithmic": f"{BYTES_PER_DOF_IT} B per DOF per Newton iteration (SURVEY 8(d) fused minimum)"},
         "kernels": {"k_newton_ms": t_newton * 1e3, "wavefront_steps": st["steps"],
                     "bicgstab_iterations": st["inner_iterations"],
-                    "k_resjac": {"ms": resjac_ms, "GB/s": resjac_gbs, "frac": resjac_gbs / peak,
-                                 "algorithmic": f"{RESJAC_BYTES_PER_DOF} B/DOF"}},
+                    "k_resjac": {"ms": resjac_ms, "GB/s": resjac_gbs, "frac": resjac_gbs / peak, "traffic": traffic_a,
+                                 "algorithmic": f"{RESJAC_BYTES_PER_DOF} B/DOF",
+                                 "kernel": "k_resjac_bulk (TMA-staged kernel a, all levels)"}},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(p.u0.nbytes + (0 if p.ring is None else p.ring.nbytes)),
                 "d2h_bytes_per_step": int(h_out.numel() * 8 + h_hist.numel() * 8), "seconds_per_step": e2e_s},
         "gpu_launches": int(launches),
