@@ -284,7 +284,9 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 const int si = sidx(hs);
                 double xN = 0.0;                       // x0 at the last own row (the halo point's S neighbour)
                 #pragma unroll
-                for (int r = 0; r < RMAX; ++r) if (r == hs - 1) xN = pp[r];
+                // (a select chain, not pp[hs - 1]: a dynamic index would move pp to local memory for the whole kernel)
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) xN = fma(r == hs - 1 ? 1.0 : 0.0, pp[r], xN);
                 hN_r0 = hN_bt - (x0c ? hN_x + hN_ci * (hN_o.e * op_s[si + 1] + hN_o.w * op_s[si - 1] +
                                                         hN_o.n * hN_x2 + hN_o.s * xN)
                                      : 0.0);
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 }
             }
             PMARK(10);
-            block_reduce2<4, 1>(a, red);
+            block_reduce2<4, 1, false>(a, red);
             if (tid == 0) {
                 double* pq = S.part + ((long long)set * G + g) * NPART;
                 pq[0] = a[0];
@@ -327,12 +329,11 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             }
         }
         PMARK(0);
-        bar_sync(S.bs, G, ep, true, hi);
-        PMARK(4);
         double bnorm2, rho, r0v0;
         {
             double o[3];
-            pair_reduce2<3, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+            bar_sync_reduce<3, 0>(S.bs, G, ep, true, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+            PMARK(4);
             rho = o[0];                                // (r^0, r0) = ||r0||^2
             bnorm2 = o[1];                             // ||b~||^2: reference of the relative stopping test
             r0v0 = o[2];                               // (r^0, v0)
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     }
                     pending = false;
                 }
-                block_reduce2<2, 2>(a, red);
+                block_reduce2<2, 2, false>(a, red);
                 if (tid == 0) {
                     if (do_p1) S.part[((long long)set * G + g) * NPART] = a[0];
                     if (do_epi) {
@@ -428,11 +429,11 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 }
                 if (do_epi) epi_done = true;
                 PMARK(1);
-                const bool any = bar_sync(S.bs, G, ep, !conv, hi);
+                double o1[1];
+                const bool any = bar_sync_reduce<1, 0>(S.bs, G, ep, !conv, hi, S.part + (long long)set * G * NPART, NPART,
+                                                       g0, g1, o1, s_red);
                 PMARK(4);
                 if (!any) { set ^= 1; break; }
-                double o1[1];
-                pair_reduce2<1, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o1, s_red);
                 const double r0v = o1[0];
                 PMARK(5);
                 set ^= 1;
@@ -486,18 +487,17 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                         }
                     }
                 }
-                block_reduce2<5, 0>(a, red);
+                block_reduce2<5, 0, false>(a, red);
                 if (tid == 0 && !conv) {
                     double* pq = S.part + ((long long)set * G + g) * NPART;
                     for (int j = 0; j < 5; ++j) pq[j] = a[j];
                 }
                 PMARK(2);
             }
-            bar_sync(S.bs, G, ep, false, hi);
-            PMARK(4);
             {
                 double o[5];
-                pair_reduce2<5, 0>(S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+                bar_sync_reduce<5, 0>(S.bs, G, ep, false, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+                PMARK(4);
                 if (!conv) {
                     const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];
                     ++it;
