@@ -345,7 +345,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     if ((rc = dalloc(h, &h->U, (size_t)(h->B * N))) ||
         (rc = dalloc(h, &h->slots, (size_t)(D * NVEC * P.ns))) ||
         (rc = dalloc(h, &h->part, (size_t)(2 * h->G * NPART))) ||
-        (rc = dalloc(h, &h->hpart, (size_t)(2 * h->G * 4))) ||
+        (rc = dalloc(h, &h->hpart, (size_t)(std::max(2, D) * h->G * 4))) ||
         (rc = dalloc(h, &h->bar, 1)) ||
         (rc = dalloc(h, &h->hist, (size_t)(4 * c.newton_max))) ||
         (rc = dalloc(h, &h->info, 2)) ||
