@@ -174,7 +174,8 @@ static const void* onchip_fn_t(int ppt) {
 
 template <bool TR, int LAW>
 static const void* col_fn_t(int rmax) {
-    return rmax <= 4 ? (const void*)k_newton_col<4, TR, LAW> : (const void*)k_newton_col<8, TR, LAW>;
+    return rmax <= 4 ? (const void*)k_newton_col<4, TR, LAW>
+                     : (rmax <= 7 ? (const void*)k_newton_col<7, TR, LAW> : (const void*)k_newton_col<8, TR, LAW>);
 }
 
 static const void* col_fn(int rmax, bool trace, int law) {
@@ -280,7 +281,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
             if (C < 1) continue;
             const int hmax = (P.nyu + C - 1) / C;
             const int rows = (hmax + Gr - 1) / Gr;
-            const int rmax = rows <= 4 ? 4 : (rows <= 8 ? 8 : 0);
+            const int rmax = rows <= 4 ? 4 : (rows <= 7 ? 7 : (rows <= 8 ? 8 : 0));
             if (!rmax) continue;
             const size_t smem = (size_t)((2 * hmax + 4) * (P.nxu + 2) + (law == 1 ? 4 : 5) * rmax * BLOCK3) * sizeof(double);
             if (smem > 220 * 1024) continue;
