@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     __shared__ double red[NWARP2 * NPART];
     __shared__ double s_hp_big[4 * GMAX2];
     __shared__ double s_red[5 * GMAX2 + 8];
-    __shared__ double hacc[MAXD][4];
+    __shared__ double lacc[MAXD][4];                   // this CTA's norm partials per pipeline slot, summed over levels
+    __shared__ double pro_s2, pro_mx, epi_s2, epi_mx;  // thread 0: this CTA's residual / update partials of the step
     __shared__ double prevmax_s;
     if (tid == 0) {
         const int D = S.D;
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         }
         prevmax_s = INFINITY;
     }
-    if (tid < MAXD * 4) hacc[tid / 4][tid % 4] = 0.0;
+    if (tid < MAXD * 4) lacc[tid / 4][tid % 4] = 0.0;
     __syncthreads();
 
     unsigned ep = 0;
@@ -90,7 +91,6 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         const double* uprev = n == 1 ? S.u0 : Ulev - ns;
         const double* ringn = S.ring ? S.ring + (long long)(n - 1) * P.ring_len : nullptr;
         double* Unew = S.mode == 1 ? nullptr : S.U + ((long long)nbuf * P.nt + (n - 1)) * ns;
-        double* hp = S.hpart + (long long)(step & 1) * G * 4;
         // this thread's sub-strip of rows [R0, R1) (strip-local), column col
         const int R0 = grp * h / Gr, R1 = (grp + 1) * h / Gr;
         const int hs = R1 - R0;
@@ -324,8 +324,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 pq[0] = a[0];
                 pq[1] = a[2];
                 pq[2] = a[3];
-                hp[g * 4 + 0] = a[1];
-                hp[g * 4 + 1] = a[4];
+                pro_s2 = a[1];
+                pro_mx = a[4];
             }
         }
         PMARK(0);
@@ -422,8 +422,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 if (tid == 0) {
                     if (do_p1) S.part[((long long)set * G + g) * NPART] = a[0];
                     if (do_epi) {
-                        hp[g * 4 + 2] = a[1];
-                        hp[g * 4 + 3] = a[2];
+                        epi_s2 = a[1];
+                        epi_mx = a[2];
                         if (a[3] != 0.0) atomicOr(&S.bs->err, 1u);
                     }
                 }
@@ -529,17 +529,33 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             PMARK(5);
         }
 
-        // ---- norms of the finished levels -> per-iteration accumulators; stop rule --------------------
-        const unsigned err = *((volatile unsigned*)&S.bs->err);
+        // ---- norms: every CTA accumulates its own partials per pipeline slot over the levels it serves; only
+        // when an iteration finishes (at most one per step: start steps are distinct) are the accumulators
+        // published and reduced over the grid (one extra barrier per iteration), then the stop rule -----------
         int stop_status = 2, stop_k = -1;
-        {
-            for (int j = tid; j < G * 4; j += BLOCK3) s_hp_big[j] = __ldcg(hp + j);
+        int kc = -1;
+        if (S.mode == 0)
+            for (int aa = 0; aa < A; ++aa)
+                if (step - sS[ks[aa]] + 1 == P.nt) kc = ks[aa];
+        if (S.mode == 0 && tid == 0) {
+            const int so = kme % S.D;
+            lacc[so][0] += pro_s2; lacc[so][1] = fmax(lacc[so][1], pro_mx);
+            lacc[so][2] += epi_s2; lacc[so][3] = fmax(lacc[so][3], epi_mx);
+            if (kc >= 0) {
+                const int sa = kc % S.D;
+                double* hq = S.hpart + ((long long)sa * G + g) * 4;
+                for (int j = 0; j < 4; ++j) { hq[j] = lacc[sa][j]; lacc[sa][j] = 0.0; }
+            }
+        }
+        if (kc >= 0) {
+            bar_sync(S.bs, G, ep, false, hi);
+            const double* hq = S.hpart + (long long)(kc % S.D) * G * 4;
+            for (int j = tid; j < G * 4; j += BLOCK3) s_hp_big[j] = __ldcg(hq + j);
             __syncthreads();
-            const int w = tid >> 5, lane = tid & 31;
-            if (w < A) {
-                const int ga0 = (int)((long long)w * G / A), ga1 = (int)((long long)(w + 1) * G / A);
+            __shared__ int s_stop[3];                  // stop_status, stop_k, last_done (thread 0 -> all)
+            if (tid < 32) {
                 double a4[4] = {0.0, 0.0, 0.0, 0.0};
-                for (int gg = ga0 + lane; gg < ga1; gg += 32) {
+                for (int gg = tid; gg < G; gg += 32) {
                     a4[0] += s_hp_big[gg * 4 + 0]; a4[1] = fmax(a4[1], s_hp_big[gg * 4 + 1]);
                     a4[2] += s_hp_big[gg * 4 + 2]; a4[3] = fmax(a4[3], s_hp_big[gg * 4 + 3]);
                 }
@@ -550,43 +566,29 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     a4[2] += __shfl_xor_sync(0xffffffffu, a4[2], o);
                     a4[3] = fmax(a4[3], __shfl_xor_sync(0xffffffffu, a4[3], o));
                 }
-                if (lane == 0) for (int j = 0; j < 4; ++j) red[w * 4 + j] = a4[j];
-            }
-            __syncthreads();
-        }
-        __shared__ int s_stop[3];                      // stop_status, stop_k, last_done (thread 0 -> all)
-        if (tid == 0) {
-            int st_ = 2, sk_ = -1, ld_ = last_done;
-            for (int a = 0; a < A; ++a) {
-                const double o[4] = {red[a * 4 + 0], red[a * 4 + 1], red[a * 4 + 2], red[a * 4 + 3]};
-                const int k = ks[a];
-                const int na = S.mode == 1 ? 1 : step - sS[k] + 1;
-                const int sa = k % S.D;
-                if (na == 1) { hacc[sa][0] = hacc[sa][1] = hacc[sa][2] = hacc[sa][3] = 0.0; }
-                hacc[sa][0] += o[0]; hacc[sa][1] = fmax(hacc[sa][1], o[1]);
-                hacc[sa][2] += o[2]; hacc[sa][3] = fmax(hacc[sa][3], o[3]);
-                if (S.mode == 0 && na == P.nt) {          // iteration k complete: record and test
-                    ld_ = k;
+                if (tid == 0) {
+                    const int k = kc;
+                    int st_ = 2, sk_ = -1;
                     const double Ntot = (double)ns * (double)P.nt;
-                    const double dmax = S.stop_norm ? sqrt(hacc[sa][2] / Ntot) : hacc[sa][3];   // stop norm
+                    const double dmax = S.stop_norm ? sqrt(a4[2] / Ntot) : a4[3];   // stop norm
                     if (g == 0) {
-                        S.hist[4 * k + 0] = sqrt(hacc[sa][0] / Ntot);
-                        S.hist[4 * k + 1] = hacc[sa][1];
-                        S.hist[4 * k + 2] = sqrt(hacc[sa][2] / Ntot);
-                        S.hist[4 * k + 3] = hacc[sa][3];
+                        S.hist[4 * k + 0] = sqrt(a4[0] / Ntot);
+                        S.hist[4 * k + 1] = a4[1];
+                        S.hist[4 * k + 2] = sqrt(a4[2] / Ntot);
+                        S.hist[4 * k + 3] = a4[3];
                     }
                     if (dmax <= S.newton_tol) { st_ = 0; sk_ = k; }
                     else if (k >= 1 && dmax > 0.5 * prevmax_s && dmax <= 1e3 * S.newton_tol) { st_ = 1; sk_ = k; }
                     else if (k + 1 >= newton_max) { st_ = -4; sk_ = k; }
                     prevmax_s = dmax;
+                    s_stop[0] = st_; s_stop[1] = sk_; s_stop[2] = k;
                 }
             }
-            s_stop[0] = st_; s_stop[1] = sk_; s_stop[2] = ld_;
+            __syncthreads();
+            stop_status = s_stop[0];
+            stop_k = s_stop[1];
+            last_done = s_stop[2];
         }
-        __syncthreads();
-        stop_status = s_stop[0];
-        stop_k = s_stop[1];
-        last_done = s_stop[2];
         if (g == 0 && tid == 0) total_inner += maxit_step;
         if (c == 0 && tid == 0 && S.stats && S.mode == 0) {
             atomicAdd((unsigned long long*)&S.stats[4], (unsigned long long)it);
@@ -596,12 +598,13 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         if (S.mode == 1) {
             if (g == 0 && tid == 0) {
                 S.info[0] = maxit_step;
-                S.info[1] = err ? -5 : 0;
+                S.info[1] = *((volatile unsigned*)&S.bs->err) ? -5 : 0;
             }
             flush_prof();
             return;
         }
-        if (err && stop_status == 2) { stop_status = -5; stop_k = last_done; }
+        // errors are raised only between a step's first and last barrier, so every CTA reads the same value here
+        if (kc >= 0 && stop_status == 2 && *((volatile unsigned*)&S.bs->err)) { stop_status = -5; stop_k = last_done; }
         if (stop_status != 2) {
             const int kf = stop_k + 1;
             const double* Uf = S.U + (long long)(kf % S.B) * P.nt * ns;
