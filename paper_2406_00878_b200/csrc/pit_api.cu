@@ -38,7 +38,8 @@ struct pit_handle {
     double* U = nullptr;          // [B][nt][ns]
     double* slots = nullptr;      // [D][NVEC][ns]
     double* part = nullptr;       // [2][G][NPART]
-    double* hpart = nullptr;      // [2][G][4]
+    double* hpart = nullptr;      // [max(2, D)][G][4]
+    double* halo = nullptr;       // engine 3: [G][2][6][512] published strip boundary rows
     GridBar* bar = nullptr;
     double* hist = nullptr;       // [newton_max][4]
     int* info = nullptr;          // [2]
@@ -137,7 +138,7 @@ static int validate(const pit_config* c, char* why, size_t n) {
 
 static void free_all(pit_handle* h) {
     for (auto& e : h->ev) if (e) { cudaEventDestroy(e); e = nullptr; }
-    cudaFree(h->U); cudaFree(h->slots); cudaFree(h->part); cudaFree(h->hpart); cudaFree(h->bar);
+    cudaFree(h->U); cudaFree(h->slots); cudaFree(h->part); cudaFree(h->hpart); cudaFree(h->halo); cudaFree(h->bar);
     cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
     cudaFree(h->d_small); cudaFree(h->bs); cudaFree(h->trace);
     cudaFree(h->pf_Y); cudaFree(h->pf_R); cudaFree(h->pf_dU); cudaFree(h->pf_part);
@@ -145,6 +146,7 @@ static void free_all(pit_handle* h) {
     h->c_u0 = h->c_ring = h->c_U = h->c_fac = nullptr; h->c_info = nullptr;
     if (h->coarse) { pit_destroy(h->coarse); h->coarse = nullptr; }
     h->bs = nullptr; h->trace = nullptr; h->pf_Y = h->pf_R = h->pf_dU = h->pf_part = nullptr;
+    h->halo = nullptr;
     h->U = h->slots = h->part = h->hpart = h->hist = h->d_u0 = h->d_bc = h->d_small = nullptr;
     h->bar = nullptr; h->info = nullptr; h->stats = nullptr;
 }
@@ -347,6 +349,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         (rc = dalloc(h, &h->slots, (size_t)(D * NVEC * P.ns))) ||
         (rc = dalloc(h, &h->part, (size_t)(2 * h->G * NPART))) ||
         (rc = dalloc(h, &h->hpart, (size_t)(std::max(2, D) * h->G * 4))) ||
+        (h->engine == 3 && (rc = dalloc(h, &h->halo, (size_t)h->G * HALO_CTA))) ||
         (rc = dalloc(h, &h->bar, 1)) ||
         (rc = dalloc(h, &h->hist, (size_t)(4 * c.newton_max))) ||
         (rc = dalloc(h, &h->info, 2)) ||
@@ -460,6 +463,7 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
         S.bs = h->bs;
         S.trace = h->trace;
         S.x0carry = getenv("PIT_X0") ? atoi(getenv("PIT_X0")) : 1;   // default: start from du^{n-1}
+        S.halo = h->halo;
         if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 13 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
         CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));

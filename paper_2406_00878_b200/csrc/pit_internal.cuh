@@ -72,6 +72,7 @@ struct SolveParams {
     struct BarState* bs;         // on-chip engine: monotonic barrier state
     unsigned long long* trace;   // optional cycle accounting [7] (nullptr = off)
     int x0carry;                 // on-chip engine: start each level solve from du^{n-1} (else 0)
+    double* halo;                // column engine: [G][2 sides][6 vectors][512] published boundary rows
     int stop_norm;               // 0: stop on max|dU_k|; 1: on the RMS update norm
 };
 

@@ -14,6 +14,9 @@
 namespace pit {
 
 constexpr int BLOCK3 = 512;
+constexpr int HALO_ROW = 512;                          // doubles per published row (nx <= 512)
+constexpr int HALO_CTA = 2 * 6 * HALO_ROW;             // per CTA: {top, bottom} x {s, t, p, v, r, v2}
+enum { HV_S = 0, HV_T = 1, HV_P = 2, HV_V = 3, HV_R = 4, HV_V2 = 5 };
 
 template <int RMAX, bool TRACE, int LAW>
 __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
@@ -81,9 +84,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         const int slot = kme % S.D;
         const int buf = kme % S.B, nbuf = (kme + 1) % S.B;
         const Slot sl = slot_at(S.slotmem, ns, slot);
-        double* const pBT = sl.bt;  double* const pX = sl.x;
-        double* const pS = sl.s;    double* const pT = sl.t;  double* const pP = sl.p[0];  double* const pV = sl.v[0];
-        double* const pR = sl.r;    double* const pV2 = sl.v[1];
+        double* const pX = sl.x;
         const int c = g - g0, C = g1 - g0;
         const int r0 = c * nyu / C, r1 = (c + 1) * nyu / C;                // 32-bit: C * nyu < 2^31
         const int h = r1 - r0;
@@ -97,6 +98,15 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         const bool own_top = R0 == 0, own_bot = R1 == h;          // sub-strip touches the CTA's halo rows
         const bool top_valid = P.bc == 1 || r0 > 0, bot_valid = P.bc == 1 || r1 < nyu;
         const int top_row = r0 == 0 ? nyu - 1 : r0 - 1, bot_row = r1 == nyu ? 0 : r1;
+        // published boundary rows: own {top, bottom} slots, and the bottom slot of the CTA owning row r0 - 1 /
+        // the top slot of the CTA owning row r1 (owner of row x in the pair: ((x + 1) C - 1) / nyu)
+        double* const hb_own = S.halo + (long long)g * HALO_CTA + col;
+        const double* const hb_S = S.halo + (long long)(g0 + ((top_row + 1) * C - 1) / nyu) * HALO_CTA + 6 * HALO_ROW + col;
+        const double* const hb_N = S.halo + (long long)(g0 + ((bot_row + 1) * C - 1) / nyu) * HALO_CTA + col;
+        auto pub = [&](int R, int v, double val) {     // row R of the strip is a boundary row: publish
+            if (R == 0) hb_own[v * HALO_ROW] = val;
+            if (R == h - 1) hb_own[(6 + v) * HALO_ROW] = val;
+        };
         const long long qc = (long long)(r0 + R0) * nxu + col;      // global index of the sub-strip's first point
         auto q_of = [&](int r) { return qc + (long long)r * nxu; };
         auto sidx = [&](int r) { return (R0 + r + 1) * W + col + 1; };   // op_s index of own point r
@@ -312,10 +322,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 v_s[r * BLOCK3 + tid] = vv;
                 a[3] += sr[r] * vv;
                 const int R = R0 + r;
-                if (R == 0 || R == h - 1) {
-                    pR[q_of(r)] = sr[r];
-                    pV2[q_of(r)] = vv;
-                }
+                if (R == 0 || R == h - 1) { pub(R, HV_R, sr[r]); pub(R, HV_V2, vv); }
             }
             PMARK(10);
             block_reduce2<4, 1, false>(a, red);
@@ -363,12 +370,12 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 if (do_p1) {
                     double hS[4] = {0.0, 0.0, 0.0, 0.0}, hN[4] = {0.0, 0.0, 0.0, 0.0};
                     if (hasS) {
-                        const long long q = (long long)top_row * nxu + col;
-                        hS[0] = __ldcg(pS + q); hS[1] = __ldcg(pT + q); hS[2] = __ldcg(pP + q); hS[3] = __ldcg(pV + q);
+                        hS[0] = __ldcg(hb_S + HV_S * HALO_ROW); hS[1] = __ldcg(hb_S + HV_T * HALO_ROW);
+                        hS[2] = __ldcg(hb_S + HV_P * HALO_ROW); hS[3] = __ldcg(hb_S + HV_V * HALO_ROW);
                     }
                     if (hasN) {
-                        const long long q = (long long)bot_row * nxu + col;
-                        hN[0] = __ldcg(pS + q); hN[1] = __ldcg(pT + q); hN[2] = __ldcg(pP + q); hN[3] = __ldcg(pV + q);
+                        hN[0] = __ldcg(hb_N + HV_S * HALO_ROW); hN[1] = __ldcg(hb_N + HV_T * HALO_ROW);
+                        hN[2] = __ldcg(hb_N + HV_P * HALO_ROW); hN[3] = __ldcg(hb_N + HV_V * HALO_ROW);
                     }
                     #pragma unroll
                     for (int r = 0; r < RMAX; ++r) {
@@ -395,10 +402,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                         v_s[r * BLOCK3 + tid] = vv;
                         a[0] += BT(r) * vv;
                         const int R = R0 + r;
-                        if (R == 0 || R == h - 1) {
-                            pR[q_of(r)] = sr[r];
-                            pV2[q_of(r)] = vv;
-                        }
+                        if (R == 0 || R == h - 1) { pub(R, HV_R, sr[r]); pub(R, HV_V2, vv); }
                     }
                 } else if (do_epi) {
                     #pragma unroll
@@ -452,14 +456,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // (t,s) (t,t) (b~,s) (b~,t) (s,s)
                 if (!conv) {
                     double hS[2] = {0.0, 0.0}, hN[2] = {0.0, 0.0};
-                    if (hasS) {
-                        const long long q = (long long)top_row * nxu + col;
-                        hS[0] = __ldcg(pR + q); hS[1] = __ldcg(pV2 + q);
-                    }
-                    if (hasN) {
-                        const long long q = (long long)bot_row * nxu + col;
-                        hN[0] = __ldcg(pR + q); hN[1] = __ldcg(pV2 + q);
-                    }
+                    if (hasS) { hS[0] = __ldcg(hb_S + HV_R * HALO_ROW); hS[1] = __ldcg(hb_S + HV_V2 * HALO_ROW); }
+                    if (hasN) { hN[0] = __ldcg(hb_N + HV_R * HALO_ROW); hN[1] = __ldcg(hb_N + HV_V2 * HALO_ROW); }
                     #pragma unroll
                     for (int r = 0; r < RMAX; ++r) {
                         if (r >= hs) continue;
@@ -482,8 +480,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                         a[0] += t * sv; a[1] += t * t; a[2] += b0 * sv; a[3] += b0 * t; a[4] += sv * sv;
                         const int R = R0 + r;
                         if (R == 0 || R == h - 1) {
-                            const long long q = q_of(r);
-                            pS[q] = sv; pT[q] = t; pP[q] = pp[r]; pV[q] = v_s[r * BLOCK3 + tid];
+                            pub(R, HV_S, sv); pub(R, HV_T, t); pub(R, HV_P, pp[r]); pub(R, HV_V, v_s[r * BLOCK3 + tid]);
                         }
                     }
                 }
