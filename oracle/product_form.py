@@ -108,3 +108,65 @@ def eq15_max_levels(N, mu, c=1.0, eps=1e-16, nt_max=100000):
         else:
             break
     return best
+
+
+# ---- N3: the paper's own explicit variant ---------------------------------------------
+
+def bandwidths(M, tol=0.0):
+    """(lower, upper) bandwidth of M: max i - j and max j - i over entries with |m_ij| > tol."""
+    ii, jj = np.nonzero(np.abs(M) > tol)
+    if len(ii) == 0:
+        return 0, 0
+    return int(max(0, (ii - jj).max())), int(max(0, (jj - ii).max()))
+
+
+def band_lu_nopivot(M, wl, wu):
+    """LU factorisation WITHOUT pivoting of a banded matrix with lower/upper bandwidths wl/wu: the paper's
+    "standard direct solver for banded matrices without pivoting" (§8).  Doolittle elimination
+    in the textbook order: for k = 0..n-1, l_ik = m_ik / m_kk for i = k+1..k+wl, then m_ij -= l_ik m_kj for
+    j = k+1..k+wu.  Returns dense (L unit lower, U upper).  No pivoting means a zero pivot yields inf/nan
+    (breakdown), exactly like the solver the paper names."""
+    A = np.array(M, dtype=np.float64, copy=True)
+    n = A.shape[0]
+    L = np.eye(n)
+    for k in range(n):
+        i1 = min(n, k + wl + 1)
+        j1 = min(n, k + wu + 1)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            l = A[k + 1:i1, k] / A[k, k]
+        L[k + 1:i1, k] = l
+        A[k + 1:i1, k] = 0.0
+        A[k + 1:i1, k + 1:j1] -= np.outer(l, A[k, k + 1:j1])
+    return L, np.triu(A)
+
+
+def band_solve_nopivot(L, U, b, wl, wu):
+    """Forward substitution with the unit lower band factor, then back substitution with the upper one."""
+    n = len(b)
+    y = np.array(b, dtype=np.float64, copy=True)
+    for k in range(n):
+        i1 = min(n, k + wl + 1)
+        y[k + 1:i1] -= L[k + 1:i1, k] * y[k]
+    x = y
+    for k in range(n - 1, -1, -1):
+        x[k] /= U[k, k]
+        i0 = max(0, k - wu)
+        x[i0:k] -= U[i0:k, k] * x[k]
+    return x
+
+
+def explicit_product_solve(A_list, r_list, diag_scaling=True):
+    """The paper's explicit form of Theorem 1: P^n and r~^n by the recursions of §5
+    (PAPER.md:221-230), the §7 diagonal preconditioner diag(P^n) applied on the left (DESIGN R11),
+    and every decoupled system solved by the banded LU without pivoting over P^n's own band."""
+    P, rt = product_form(A_list, r_list)
+    out = []
+    for Pn, rn in zip(P, rt):
+        M, b = Pn, rn
+        if diag_scaling:
+            d = np.diag(Pn).copy()
+            M, b = Pn / d[:, None], rn / d
+        wl, wu = bandwidths(M)
+        L, U = band_lu_nopivot(M, wl, wu)
+        out.append(band_solve_nopivot(L, U, b, wl, wu))
+    return out
