@@ -61,7 +61,11 @@ typedef enum {
 
 enum { PIT_HEAT = 0, PIT_BURGERS = 1 };                 /* PAPER.md:52 */
 enum { PIT_DIRICHLET = 0, PIT_PERIODIC = 1 };           /* Eq. (2) PAPER.md:54-61; periodic = extension */
-enum { PIT_INV_AUTO = 0, PIT_INV_RECURRENCE = 1, PIT_INV_PRODUCT_WINDOW = 2 };
+/* Inversion of the block-bidiagonal Newton matrix of Eq. (6): AUTO, the on-device level recurrence of Eq. (7)
+ * (default fast path), the Theorem 1 product form with nested level solves inside the Section 7 gate (b2), or
+ * the paper's explicit form — banded P^n by Eq. (10), diag(P^n) scaling (PAPER.md:337), banded LU without
+ * pivoting (PAPER.md:342); Dirichlet only, no gate; window = 0 means the whole horizon (N3) */
+enum { PIT_INV_AUTO = 0, PIT_INV_RECURRENCE = 1, PIT_INV_PRODUCT_WINDOW = 2, PIT_INV_EXPLICIT = 3 };
 
 typedef struct {
     int32_t abi_version;   /* must equal PIT_ABI_VERSION */
@@ -79,7 +83,8 @@ typedef struct {
     double  lin_atol;      /* ... or RMS(b~ - A~ x) = ||.||_2 / sqrt(ns) <= lin_atol; 0 = default 1e-4 * newton_tol */
     int32_t lin_max;       /* per-level BiCGSTAB iteration cap; 0 = default 1000 */
     int32_t inverse_mode;  /* PIT_INV_*; AUTO = recurrence unless the product window admits all levels */
-    int32_t window;        /* product-form window length; 0 = auto from the Section 7 gate */
+    int32_t window;        /* product-form window length; 0 = auto from the Section 7 gate (PRODUCT_WINDOW) or
+                              the whole horizon (EXPLICIT) */
     int32_t pipeline_depth;/* Newton iterations in flight in the level wavefront; 0 = auto */
     int32_t device;        /* CUDA device ordinal */
     int32_t engine;        /* 0 = auto (column-blocked on-chip if it fits, else strip on-chip, else global),
@@ -151,6 +156,18 @@ int pit_product_window_device(pit_handle* h, int32_t s0, int32_t L, const double
                               const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
                               int32_t* d_info, void* cuda_stream);
 
+/* N3 on its own, for tests: the paper's explicit decoupled form for levels [s0, s0+L) of the device iterate
+ * (Theorem 1, PAPER.md:169-184): P^1 = A_{s0}, P^m = P^{m-1} A_{s0+m-1} formed in band storage (Eq. 10,
+ * PAPER.md:221-230; half-bandwidth m * nxu, Theorem 2), r~^m = sum_{j<=m} P^{j-1} r^j with r^1 += d_carry, the
+ * diagonal preconditioner diag(P^m) on the left (PAPER.md:337), and each P^m du^m = r~^m solved by a banded LU
+ * WITHOUT pivoting (PAPER.md:342).  Arguments as pit_product_window_device; no conditioning gate (this is the
+ * path that exhibits the Section 7 limit).  d_info [2] = { 0, PIT_OK | PIT_EBREAKDOWN (zero / non-finite
+ * pivot) } on the device.  Errors: PIT_EINVAL for periodic grids (P^n is not banded) or band storage
+ * L * ns * (2w+1) doubles > 16 GB; PIT_ENOMEM.  The handle owns the band scratch (grown on demand). */
+int pit_explicit_window_device(pit_handle* h, int32_t s0, int32_t L, const double* d_U, const double* d_u0,
+                               const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
+                               int32_t* d_info, void* cuda_stream);
+
 /* The initial Newton iterate on its own (PAPER.md:214-215): with guess_cf >= 2 the coarse-grid solve + spline
  * interpolation described at pit_config.guess_cf, else u^0 at every level; written to d_U0 [nt][ns] (device).
  * d_u0 [ns], d_bc as in pit_solve_device.  Asynchronous on cuda_stream. */
@@ -168,7 +185,7 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * (prologue, phase 1, phase 2, epilogue, grid barriers, scalar reductions, step bookkeeping) when the
  * environment variable PIT_TRACE was set at pit_create (zeros otherwise), out[15] = 1 if the last solve
  * inverted Eq. (6) with the (b2) product form (inverse_mode PRODUCT_WINDOW, or AUTO with the whole horizon
- * inside the Section 7 gate), 0 for the on-device level recurrence, out[16] = BiCGSTAB iterations summed
+ * inside the Section 7 gate), 2 with the N3 explicit banded form, 0 for the on-device level recurrence, out[16] = BiCGSTAB iterations summed
  * over all (level, iteration) pairs (on-chip engine), out[17 + k] = those of Newton iteration k,
  * out[273..278] = prologue sub-categories of the cycle accounting, out[279] = device time of the coarse-grid
  * initial guess (coarse solve + interpolation) [ns], 0 without it. */

@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpit.so")
-SOURCES = ["pit_api.cu", "pit_kernels.cu", "pit_internal.cuh", "pit_newton_onchip.cuh", "pit_newton_col.cuh", "pit_guess.cuh"]
+SOURCES = ["pit_api.cu", "pit_kernels.cu", "pit_internal.cuh", "pit_newton_onchip.cuh", "pit_newton_col.cuh", "pit_guess.cuh", "pit_explicit.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 

@@ -18,6 +18,7 @@
 
 #include "pit_kernels.cu"
 #include "pit_guess.cuh"
+#include "pit_explicit.cuh"
 
 using namespace pit;
 
@@ -34,7 +35,11 @@ struct pit_handle {
     double* pf_R = nullptr;       // (b2) host-driven Newton: residuals [nt][ns]
     double* pf_dU = nullptr;      // (b2) host-driven Newton: update [nt][ns]
     double* pf_part = nullptr;    // (b2) partials
-    bool product_used = false;    // last solve used the (b2) product-form path
+    int product_used = 0;         // last solve: 0 level recurrence, 1 (b2) product form, 2 N3 explicit banded form
+    double* ex_B = nullptr;       // N3: band storage of P^1..P^L of a window [L][ns][2w+1]
+    double* ex_C5 = nullptr;      // N3: coefficients of A_{s0..s0+L-1} [L][5][ns]
+    long long ex_capB = 0, ex_capC = 0;
+    unsigned* ex_err = nullptr;   // N3: zero / non-finite pivot flag
     double* U = nullptr;          // [B][nt][ns]
     double* slots = nullptr;      // [D][NVEC][ns]
     double* part = nullptr;       // [2][G][NPART]
@@ -123,7 +128,11 @@ static int validate(const pit_config* c, char* why, size_t n) {
     if (!(c->newton_tol > 0.0)) { snprintf(why, n, "newton_tol must be > 0"); return PIT_EINVAL; }
     if (c->newton_max < 1 || c->newton_max > MAXK) { snprintf(why, n, "newton_max must be in 1..%d", MAXK); return PIT_EINVAL; }
     if (c->lin_rtol < 0.0 || c->lin_atol < 0.0 || c->lin_max < 0) { snprintf(why, n, "negative solver tolerance"); return PIT_EINVAL; }
-    if (c->inverse_mode < 0 || c->inverse_mode > 2) { snprintf(why, n, "inverse_mode %d", c->inverse_mode); return PIT_EINVAL; }
+    if (c->inverse_mode < 0 || c->inverse_mode > 3) { snprintf(why, n, "inverse_mode %d", c->inverse_mode); return PIT_EINVAL; }
+    if (c->inverse_mode == PIT_INV_EXPLICIT && c->bc != PIT_DIRICHLET) {
+        snprintf(why, n, "inverse_mode EXPLICIT needs Dirichlet boundaries (the periodic wrap makes P^n non-banded)");
+        return PIT_EINVAL;
+    }
     if (c->pipeline_depth < 0 || c->pipeline_depth > MAXD) { snprintf(why, n, "pipeline_depth must be in 0..%d", MAXD); return PIT_EINVAL; }
     if (c->window < 0) { snprintf(why, n, "window < 0"); return PIT_EINVAL; }
     if (c->stop_norm < 0 || c->stop_norm > 1) { snprintf(why, n, "stop_norm %d", c->stop_norm); return PIT_EINVAL; }
@@ -142,6 +151,8 @@ static void free_all(pit_handle* h) {
     cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
     cudaFree(h->d_small); cudaFree(h->bs); cudaFree(h->trace);
     cudaFree(h->pf_Y); cudaFree(h->pf_R); cudaFree(h->pf_dU); cudaFree(h->pf_part);
+    cudaFree(h->ex_B); cudaFree(h->ex_C5); cudaFree(h->ex_err);
+    h->ex_B = h->ex_C5 = nullptr; h->ex_err = nullptr; h->ex_capB = h->ex_capC = 0;
     cudaFree(h->c_u0); cudaFree(h->c_ring); cudaFree(h->c_U); cudaFree(h->c_fac); cudaFree(h->c_info);
     h->c_u0 = h->c_ring = h->c_U = h->c_fac = nullptr; h->c_info = nullptr;
     if (h->coarse) { pit_destroy(h->coarse); h->coarse = nullptr; }
@@ -501,6 +512,8 @@ static int level_anorms(pit_handle* h, const double* d_U, const double* d_bc, in
 static double chain_bound(const double* anorm_from_s0, int L);
 static int product_window(pit_handle* h, int s0, int L, const double* d_U, const double* d_bc, const double* d_R,
                           const double* d_carry, double* d_dU, int* d_info, cudaStream_t st);
+static int explicit_window(pit_handle* h, int s0, int L, const double* d_U, const double* d_bc, const double* d_R,
+                           const double* d_carry, double* d_dU, int* d_info, cudaStream_t st);
 
 // Host-driven all-at-once Newton with the (b2) product-form inverse (inverse_mode PRODUCT_WINDOW): the same
 // iteration, initial guess, norms and stop rule as the persistent kernels, but Eq. (6) is inverted window by
@@ -519,6 +532,7 @@ static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, 
     int status = PIT_ENOCONV, kdone = 0;
     double prevmax = INFINITY;
     const int gr = std::min(grid_for(N, h->sms), 1024);
+    CUDA_TRY(h, cudaEventRecord(h->ev[2], st));      // device time of the host-driven Newton loop (pit_stats)
     for (int k = 0; k < kmax; ++k) {
         const int gpart = launch_resjac(h, gr, st, U, d_u0, ring, h->pf_R, nullptr, h->d_small);
         CUDA_TRY(h, cudaGetLastError());
@@ -528,6 +542,14 @@ static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, 
         CUDA_TRY(h, cudaMemcpyAsync(rn, h->d_small + 2048, sizeof(rn), cudaMemcpyDeviceToHost, st));
         for (int s0 = 1; s0 <= P.nt;) {
             int L;
+            if (h->cfg.inverse_mode == PIT_INV_EXPLICIT) {     // N3: the paper's explicit form; no gate (it is what
+                L = h->cfg.window > 0 ? std::min(h->cfg.window, P.nt - s0 + 1) : P.nt - s0 + 1;   // shows §7's limit)
+                rc = explicit_window(h, s0, L, U, d_bc, h->pf_R, s0 == 1 ? nullptr : h->pf_dU + (long long)(s0 - 2) * ns,
+                                     h->pf_dU + (long long)(s0 - 1) * ns, d_info, st);
+                if (rc != PIT_OK) return rc;
+                s0 += L;
+                continue;
+            }
             if ((rc = level_anorms(h, U, d_bc, s0, P.nt - s0 + 1, an.data(), st)) != PIT_OK) return rc;
             if (h->cfg.window > 0) {
                 L = std::min(h->cfg.window, P.nt - s0 + 1);
@@ -559,19 +581,20 @@ static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, 
         if (k >= 1 && dn > 0.5 * prevmax && dn <= 1e3 * h->cfg.newton_tol) { status = PIT_OK_FLOOR; break; }
         prevmax = dn;
     }
+    CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
     if (d_u_out) CUDA_TRY(h, cudaMemcpyAsync(d_u_out, U, sizeof(double) * N, cudaMemcpyDeviceToDevice, st));
     if (d_hist) CUDA_TRY(h, cudaMemcpyAsync(d_hist, hist.data(), sizeof(double) * 4 * kmax, cudaMemcpyHostToDevice, st));
     const int info[2] = {kdone, status};
     CUDA_TRY(h, cudaMemcpyAsync(d_info ? d_info : h->info, info, sizeof(info), cudaMemcpyHostToDevice, st));
     CUDA_TRY(h, cudaStreamSynchronize(st));
-    h->product_used = true;
+    h->product_used = h->cfg.inverse_mode == PIT_INV_EXPLICIT ? 2 : 1;
     return PIT_OK;
 }
 
 // AUTO: the paper's literal product form when the Section 7 gate admits the whole horizon as one window
 // (BASELINE c1), the recurrence otherwise.
 static bool want_product(pit_handle* h, const double* d_bc, cudaStream_t st) {
-    if (h->cfg.inverse_mode == PIT_INV_PRODUCT_WINDOW) return true;
+    if (h->cfg.inverse_mode == PIT_INV_PRODUCT_WINDOW || h->cfg.inverse_mode == PIT_INV_EXPLICIT) return true;
     if (h->cfg.inverse_mode == PIT_INV_RECURRENCE || h->P.nt > 64) return false;
     if (ensure_pf_scratch(h) != PIT_OK) return false;
     std::vector<double> an(h->P.nt);
@@ -647,7 +670,7 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
         return rc;
     }
     if (d_hist) CUDA_TRY(h, cudaMemsetAsync(d_hist, 0, sizeof(double) * 4 * h->cfg.newton_max, st));
-    h->product_used = false;
+    h->product_used = 0;
     if (want_product(h, d_bc, st)) return solve_product(h, d_u0, d_bc, d_u_out, d_hist, (int*)d_info, st);
     SolveParams S = base_params(h);
     S.u0 = d_u0;
@@ -689,7 +712,7 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     int rc = launch_init(h, h->d_u0, guess ? h->U : nullptr, 0);
     if (rc != PIT_OK) return rc;
     CUDA_TRY(h, cudaMemset(h->hist, 0, sizeof(double) * 4 * h->cfg.newton_max));
-    h->product_used = false;
+    h->product_used = 0;
     const bool prod = want_product(h, has_bc ? h->d_bc : nullptr, 0);
     if (prod) {
         rc = solve_product(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
@@ -884,7 +907,7 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     if (h->trace) CUDA_TRY(h, cudaMemcpy(tr, h->trace, sizeof(tr), cudaMemcpyDeviceToHost));
     const long long v[17] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
                              h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
-                             (long long)tr[4], (long long)tr[5], (long long)tr[6], h->product_used ? 1 : 0, s[4]};
+                             (long long)tr[4], (long long)tr[5], (long long)tr[6], (long long)h->product_used, s[4]};
     for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];
     for (int i = 17; i < n && i < 17 + MAXK; ++i) out[i] = s[8 + (i - 17)];
     for (int i = 17 + MAXK; i < n && i < 17 + MAXK + 6; ++i) out[i] = (long long)tr[7 + (i - 17 - MAXK)];
@@ -896,3 +919,85 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     return PIT_OK;
 }
 
+
+// ---- N3: the paper's explicit banded form (pit_explicit.cuh) --------------------------------------------
+
+__global__ void k_err_to_info(const unsigned* err, int* info) {
+    info[0] = 0;
+    info[1] = *err ? PIT_EBREAKDOWN : PIT_OK;
+}
+
+// du^{s0..s0+L-1} of Eq. (6) by the explicit decoupled form: A_m coefficients, P^1 = A_1 and P^m = P^{m-1} A_m
+// in band storage (Eq. 10), y^m = P^{m-1} r^m and the level scan r~^m = sum_{j<=m} y^j, the
+// §7 diagonal scaling, then one banded LU without pivoting + substitution per level.  r^1 includes the carry.
+static int explicit_window(pit_handle* h, int s0, int L, const double* d_U, const double* d_bc, const double* d_R,
+                           const double* d_carry, double* d_dU, int* d_info, cudaStream_t st) {
+    const Prob& P = h->P;
+    const long long ns = P.ns;
+    if (P.bc != PIT_DIRICHLET) return set_err(h, PIT_EINVAL, "explicit form needs Dirichlet boundaries");
+    const long long w = std::min<long long>((long long)L * P.nxu, ns - 1), BW = 2 * w + 1;
+    const long long needB = (long long)L * ns * BW, needC = (long long)L * 5 * ns;
+    if ((double)needB * 8.0 > 16e9)
+        return set_err(h, PIT_EINVAL, "explicit form: band storage of %d levels x %lld x %lld needs %.1f GB (> 16 GB)", L,
+                       ns, BW, (double)needB * 8e-9);
+    const size_t smem = (size_t)std::max<long long>(1, 2 * w) * sizeof(double);
+    if (smem > 200 * 1024) return set_err(h, PIT_EINVAL, "explicit form: half-bandwidth %lld too large", w);
+    int rc = ensure_pf_scratch(h);
+    if (rc != PIT_OK) return rc;
+    if (needB > h->ex_capB) {
+        cudaFree(h->ex_B); h->ex_B = nullptr; h->ex_capB = 0;
+        if ((rc = dalloc(h, &h->ex_B, (size_t)needB))) return rc;
+        h->ex_capB = needB;
+    }
+    if (needC > h->ex_capC) {
+        cudaFree(h->ex_C5); h->ex_C5 = nullptr; h->ex_capC = 0;
+        if ((rc = dalloc(h, &h->ex_C5, (size_t)needC))) return rc;
+        h->ex_capC = needC;
+    }
+    if (!h->ex_err) CUDA_TRY(h, cudaMalloc((void**)&h->ex_err, sizeof(unsigned)));
+    const int gx = std::max(1, std::min(grid_for(ns, h->sms), 256));
+    k_coef5<<<dim3(gx, L), BLOCK, 0, st>>>(P, d_U, d_bc, s0, h->ex_C5);
+    CUDA_TRY(h, cudaGetLastError());
+    const int gb = std::max(1, std::min(grid_for(ns * BW, h->sms), 16 * h->sms));
+    k_band_init<<<gb, BLOCK, 0, st>>>(ns, P.nxu, (int)w, h->ex_C5, h->ex_B);
+    CUDA_TRY(h, cudaGetLastError());
+    for (int m = 2; m <= L; ++m) {
+        k_band_mul<<<gb, BLOCK, 0, st>>>(ns, P.nxu, (int)w, h->ex_B + (long long)(m - 2) * ns * BW,
+                                         h->ex_C5 + (long long)(m - 1) * 5 * ns, h->ex_B + (long long)(m - 1) * ns * BW);
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    const double* Rw = d_R + (long long)(s0 - 1) * ns;
+    CUDA_TRY(h, cudaMemcpyAsync(d_dU, Rw, sizeof(double) * ns, cudaMemcpyDeviceToDevice, st));
+    if (d_carry) {   // first row of the window: A_{s0} du^{s0} = r^{s0} + du^{s0-1}
+        k_update<<<grid_for(ns, h->sms), BLOCK, 0, st>>>(ns, d_dU, d_carry, h->pf_part);
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    if (L > 1) {
+        k_band_rhs<<<dim3(gx, L - 1), BLOCK, 0, st>>>(ns, (int)w, h->ex_B, Rw, d_dU);
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    k_level_prefix<<<gx, BLOCK, 0, st>>>(ns, L, d_dU);
+    CUDA_TRY(h, cudaGetLastError());
+    k_band_scale<<<dim3(gx, L), BLOCK, 0, st>>>(ns, (int)w, h->ex_B, d_dU);
+    CUDA_TRY(h, cudaGetLastError());
+    CUDA_TRY(h, cudaMemsetAsync(h->ex_err, 0, sizeof(unsigned), st));
+    CUDA_TRY(h, cudaFuncSetAttribute(k_band_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_band_lu_solve<<<L, BLOCKX, smem, st>>>(ns, P.nxu, (int)w, h->ex_B, d_dU, h->ex_err);
+    CUDA_TRY(h, cudaGetLastError());
+    if (d_info) {
+        k_err_to_info<<<1, 1, 0, st>>>(h->ex_err, d_info);
+        CUDA_TRY(h, cudaGetLastError());
+    }
+    h->launches += 7 + (L - 1) + (d_carry ? 1 : 0) + (d_info ? 1 : 0);
+    return PIT_OK;
+}
+
+int pit_explicit_window_device(pit_handle* h, int32_t s0, int32_t L, const double* d_U, const double* d_u0,
+                               const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
+                               int32_t* d_info, void* cuda_stream) {
+    (void)d_u0;
+    if (!h || !d_U || !d_R || !d_dU) return set_err(h, PIT_EINVAL, "null argument");
+    if (s0 < 1 || L < 1 || s0 + L - 1 > h->P.nt) return set_err(h, PIT_EINVAL, "window [%d, %d) out of 1..%d", s0, s0 + L, h->P.nt);
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    return explicit_window(h, s0, L, d_U, d_bc, d_R, d_carry, d_dU, (int*)d_info, (cudaStream_t)cuda_stream);
+}

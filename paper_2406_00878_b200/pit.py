@@ -20,11 +20,11 @@ PIT_ABI_VERSION = 2
 PIT_OK, PIT_OK_FLOOR, PIT_EINVAL, PIT_ENOMEM, PIT_ECUDA, PIT_ENOCONV, PIT_EBREAKDOWN, PIT_ECOND = 0, 1, -1, -2, -3, -4, -5, -6
 PIT_HEAT, PIT_BURGERS = 0, 1
 PIT_DIRICHLET, PIT_PERIODIC = 0, 1
-PIT_INV_AUTO, PIT_INV_RECURRENCE, PIT_INV_PRODUCT_WINDOW = 0, 1, 2
+PIT_INV_AUTO, PIT_INV_RECURRENCE, PIT_INV_PRODUCT_WINDOW, PIT_INV_EXPLICIT = 0, 1, 2, 3
 
 # every symbol include/pit.h declares (tests check the library exports all of them)
 EXPORTS = ["pit_config_init", "pit_create", "pit_destroy", "pit_solve", "pit_solve_device", "pit_residual_device",
-           "pit_level_solve_device", "pit_product_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_strerror",
+           "pit_level_solve_device", "pit_product_window_device", "pit_explicit_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_strerror",
            "pit_last_error", "pit_abi_version"]
 
 
@@ -65,6 +65,8 @@ def lib():
         L.pit_level_solve_device.restype = C.c_int
         L.pit_product_window_device.argtypes = [hp, C.c_int32, C.c_int32, dp, dp, dp, dp, dp, dp, i32p, vp]
         L.pit_product_window_device.restype = C.c_int
+        L.pit_explicit_window_device.argtypes = [hp, C.c_int32, C.c_int32, dp, dp, dp, dp, dp, dp, i32p, vp]
+        L.pit_explicit_window_device.restype = C.c_int
         L.pit_initial_guess_device.argtypes = [hp, dp, dp, dp, vp]; L.pit_initial_guess_device.restype = C.c_int
         L.pit_sizes.argtypes = [hp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]; L.pit_sizes.restype = C.c_int
         L.pit_stats.argtypes = [hp, C.POINTER(C.c_int64), C.c_int32]; L.pit_stats.restype = C.c_int
@@ -164,12 +166,17 @@ class Solver:
                                                            _ptr(d_R), _ptr(d_carry), _ptr(d_dU), _ptr(d_info),
                                                            _stream(stream)))
 
+    def explicit_window_device(self, s0, L, d_U, d_u0, d_ring, d_R, d_carry, d_dU, d_info, stream=None) -> int:
+        return self._check(lib().pit_explicit_window_device(self.h, s0, L, _ptr(d_U), _ptr(d_u0), _ptr(d_ring),
+                                                            _ptr(d_R), _ptr(d_carry), _ptr(d_dU), _ptr(d_info),
+                                                            _stream(stream)))
+
     def stats(self):
         out = (C.c_int64 * (17 + 256 + 7))()
         self._check(lib().pit_stats(self.h, out, 17 + 256 + 7))
         d = {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
              "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6, "engine": out[7],
-             "product_form": bool(out[15]), "pair_iterations": out[16],
+             "product_form": bool(out[15]), "explicit_form": out[15] == 2, "pair_iterations": out[16],
              "iterations_per_newton_k": [out[17 + k] for k in range(256) if out[17 + k]],
              "guess_ms": out[279] * 1e-6}
         if any(out[8:15]):
