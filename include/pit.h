@@ -79,7 +79,8 @@ typedef struct {
     double  newton_tol;    /* stop on ||dU_k|| <= newton_tol (> 0; BASELINE: 1e-12), norm chosen by stop_norm */
     int32_t newton_max;    /* max Newton iterations (1..256) */
     double  lin_rtol;      /* per-level solve: ||b~ - A~ x||_2 <= lin_rtol ||b~||_2 (A~ = diag-scaled A_n);
-                              0 = default 1e-10 */
+                              0 = default 1e-6 (an inexact-Newton forcing term:
+                              the Newton iteration counts of BASELINE c1-c5 are those of exact solves, DESIGN R10) */
     double  lin_atol;      /* ... or RMS(b~ - A~ x) = ||.||_2 / sqrt(ns) <= lin_atol; 0 = default 1e-4 * newton_tol */
     int32_t lin_max;       /* per-level BiCGSTAB iteration cap; 0 = default 1000 */
     int32_t inverse_mode;  /* PIT_INV_*; AUTO = recurrence unless the product window admits all levels */

@@ -242,7 +242,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     if (!h) return PIT_ENOMEM;
     h->cfg = *cfg;
     pit_config& c = h->cfg;
-    if (c.lin_rtol == 0.0) c.lin_rtol = 1e-10;
+    if (c.lin_rtol == 0.0) c.lin_rtol = 1e-6;     // inexact-Newton forcing term (R10)
     if (c.lin_atol == 0.0) c.lin_atol = 1e-4 * c.newton_tol;
     if (c.lin_max == 0) c.lin_max = 1000;
 

@@ -229,12 +229,16 @@ def test_column_engine(case):
         p, m = W.paper_heat(257, nt=3), 1
     else:
         p, m = W.paper_burgers(257, mu=0.01, nt=5), 5
-    U3, h3, n3, s3, st3 = gpu_solve(p, engine=3)
+    U3, h3, n3, s3, st3 = gpu_solve(p, engine=3)             # default (inexact-Newton) inner tolerance
     assert st3["engine"] == 3 and s3 in (0, 1)
-    U1, h1, n1, s1, _ = gpu_solve(p, engine=1, inverse_mode=pit.PIT_INV_RECURRENCE)
-    assert n3 == n1 and normwise_rel(U3, U1) <= 1e-11
     seq = O.solve_sequential(p, levels=m)
     assert np.abs(U3[:m] - seq.U).max() / np.abs(seq.U).max() <= 1e-10
+    # engine equivalence with (near-)exact level solves: two BiCGSTAB implementations stopped at a loose forcing
+    # term may legitimately take different Newton iteration counts near the stop threshold (R10)
+    kw = dict(inverse_mode=pit.PIT_INV_RECURRENCE, lin_rtol=1e-13)
+    U3, h3, n3, s3, st3 = gpu_solve(p, engine=3, **kw)
+    U1, h1, n1, s1, _ = gpu_solve(p, engine=1, **kw)
+    assert n3 == n1 and normwise_rel(U3, U1) <= 1e-11
 
 
 @pytest.mark.parametrize("ny,nt,depth", [(8, 3, 0), (8, 2, 1), (16, 3, 0), (148, 3, 0), (300, 3, 0)])

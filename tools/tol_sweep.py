@@ -17,14 +17,15 @@ def run(p, **cfg):
     st = s.stats()
     nit, status = (int(v) for v in d_info.cpu())
     U = d_out.cpu().numpy()
+    h = d_hist.cpu().numpy()[:nit, 3]
     s.close()
-    return U, nit, status, st
+    return U, nit, status, st, h
 
 for c in [int(a) for a in sys.argv[1:]] or [4, 5]:
     p = W.config(c)
-    U0, n0, s0, st0 = run(p)
-    print(f"c{c} default: {st0['newton_kernel_ms']:.1f} ms its={n0} pair-sum={st0['pair_iterations']}")
-    for rt, at in [(1e-10, 0.0), (1e-13, 1e-16 * np.sqrt(p.ns)), (1e-10, 1e-16 * np.sqrt(p.ns)), (1e-8, 1e-16 * np.sqrt(p.ns))]:
-        U, n, st_, st = run(p, lin_rtol=rt, lin_atol=at)
+    U0, n0, s0, st0, h0 = run(p)
+    print(f"c{c} default: {st0['newton_kernel_ms']:.1f} ms its={n0} steps={st0['steps']} pair-sum={st0['pair_iterations']} per-k={st0['iterations_per_newton_k']} hist={np.array2string(h0, precision=1)}", flush=True)
+    for rt in [float(x) for x in os.environ.get("RTOLS", "1e-6,1e-7,1e-8,1e-9").split(",")]:
+        U, n, st_, st, h = run(p, lin_rtol=rt)
         err = np.abs(U - U0).max() / np.abs(U0).max()
-        print(f"  rtol={rt:g} atol={at:.3g}: {st['newton_kernel_ms']:.1f} ms its={n} status={st_} pair-sum={st['pair_iterations']} per-k={st['iterations_per_newton_k']} rel-diff={err:.2e}")
+        print(f"  rtol={rt:g}: {st['newton_kernel_ms']:.1f} ms its={n} status={st_} steps={st['steps']} pair-sum={st['pair_iterations']} per-k={st['iterations_per_newton_k']} rel-diff={err:.2e} hist={np.array2string(h, precision=1)}", flush=True)
