@@ -296,7 +296,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
             const int rows = (hmax + Gr - 1) / Gr;
             const int rmax = rows <= 4 ? 4 : (rows <= 7 ? 7 : (rows <= 8 ? 8 : 0));
             if (!rmax) continue;
-            const size_t smem = (size_t)((2 * hmax + 4) * (P.nxu + 2) + (law == 1 ? 4 : 5) * rmax * BLOCK3) * sizeof(double);
+            const size_t smem = (size_t)((2 * hmax + 4) * (P.nxu + 4) + (law == 1 ? 4 : 5) * rmax * BLOCK3) * sizeof(double);
             if (smem > 220 * 1024) continue;
             bool ok = true;
             int occ3 = 0;

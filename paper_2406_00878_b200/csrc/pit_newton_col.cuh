@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     const long long ns = P.ns;
     const int nxu = P.nxu, nyu = P.nyu;
     const int G = S.G, g = blockIdx.x, tid = threadIdx.x;
-    const int W = nxu + 2;
+    const int W = nxu + 4;                             // row pitch of u_s / op_s: data at +2 (16-byte aligned rows)
     const int HM = S.hmax;
     double* const u_s = smem;                          // [HM+2][W] u of the strip rows + halo rows (+ ring / wrap columns)
     double* const op_s = u_s + (HM + 2) * W;           // [HM+2][W] matvec operand (E/W exchange, halo rows)
@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         prevmax_s = INFINITY;
     }
     if (tid < MAXD * 4) lacc[tid / 4][tid % 4] = 0.0;
+    for (int i = tid; i < (HM + 2) * W; i += BLOCK3) op_s[i] = 0.0;   // Dirichlet: the dropped columns stay 0
     __syncthreads();
 
     unsigned ep = 0;
@@ -68,6 +69,10 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     const double atol2 = S.lin_atol * S.lin_atol * (double)P.ns;     // lin_atol bounds the RMS residual
     const int Gr = BLOCK3 / nxu;                       // column groups (1 or 2)
     const int col = tid % nxu, grp = tid / nxu;
+    // E / W neighbours in the u_s / op_s rows: the next column, or the periodic wrap inside the row; Dirichlet
+    // edges read the halo columns (u_s: the ring, staged every step; op_s: zeros, written once below)
+    const int dE = (P.bc == 1 && col == nxu - 1) ? -(nxu - 1) : 1;
+    const int dW = (P.bc == 1 && col == 0) ? (nxu - 1) : -1;
     const double ci_const = 1.0 / (1.0 + 2.0 * P.dt * P.m0 * (P.ihx2 + P.ihy2));   // LAW 1: a_C is constant
 
     for (int step = 1;; ++step) {
@@ -109,8 +114,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         };
         const long long qc = (long long)(r0 + R0) * nxu + col;      // global index of the sub-strip's first point
         auto q_of = [&](int r) { return qc + (long long)r * nxu; };
-        auto sidx = [&](int r) { return (R0 + r + 1) * W + col + 1; };   // op_s index of own point r
-        auto uidx = [&](int r) { return (R0 + r + 1) * W + col + 1; };   // u_s index of own point r
+        auto sidx = [&](int r) { return (R0 + r + 1) * W + col + 2; };   // op_s index of own point r
+        auto uidx = [&](int r) { return (R0 + r + 1) * W + col + 2; };   // u_s index of own point r
 
         double sr[RMAX], pp[RMAX];
         auto X = [&](int r) -> double& { return x_s[r * BLOCK3 + tid]; };
@@ -148,8 +153,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (hs == 0) break;
             const int ui = uidx(r), gr = r0 + R0 + r;
             stage_u(ui, gr, col);
-            if (col == 0) stage_u(ui - 1, gr, -1);              // W halo column: wrap or ring
-            if (col == nxu - 1) stage_u(ui + 1, gr, nxu);       // E halo column
+            if (P.bc != 1 && col == 0) stage_u(ui - 1, gr, -1);          // W halo column: the Dirichlet ring
+            if (P.bc != 1 && col == nxu - 1) stage_u(ui + 1, gr, nxu);   // E halo column
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         PMARK(12);
@@ -206,18 +211,11 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         };
         auto put_op_at = [&](int si, double val) {
             op_s[si] = val;
-            if (P.bc == 1) {
-                if (col == 0) op_s[si + nxu] = val;
-                if (col == nxu - 1) op_s[si - nxu] = val;
-            } else {
-                if (col == 0) op_s[si - 1] = 0.0;          // Dirichlet: the dropped columns stay 0
-                if (col == nxu - 1) op_s[si + 1] = 0.0;
-            }
         };
         auto put_op = [&](int r, double val) { put_op_at(sidx(r), val); };
         auto coef = [&](int r) -> Off {
             const int ui = uidx(r);
-            const Vals uv = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], u_s[ui - W]};
+            const Vals uv = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], u_s[ui - W]};
             return offdiag_law<LAW>(P, uv);
         };
         auto cinv = [&](int r) -> double { return LAW == 1 ? ci_const : ci_s[r * BLOCK3 + tid]; };
@@ -229,7 +227,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 pp[r] = 0.0;
                 if (r >= hs) continue;
                 const int ui = uidx(r);
-                const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], u_s[ui - W]};
+                const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], u_s[ui - W]};
                 double G, aC;
                 res_diag<LAW>(P, v, up[r], G, aC);
                 double rhs;
@@ -255,7 +253,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             Off hS_o = {0.0, 0.0, 0.0, 0.0}, hN_o = {0.0, 0.0, 0.0, 0.0};
             if (hasS) {
                 const int ui = uidx(-1);
-                const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], u_s[ui + W], hS_u2};
+                const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], hS_u2};
                 double G, aC;
                 res_diag<LAW>(P, v, hS_up, G, aC);
                 hS_ci = LAW == 1 ? ci_const : 1.0 / aC;
@@ -265,7 +263,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             }
             if (hasN) {
                 const int ui = uidx(hs);
-                const Vals v = {u_s[ui], u_s[ui + 1], u_s[ui - 1], hN_u2, u_s[ui - W]};
+                const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], hN_u2, u_s[ui - W]};
                 double G, aC;
                 res_diag<LAW>(P, v, hN_up, G, aC);
                 hN_ci = LAW == 1 ? ci_const : 1.0 / aC;
@@ -281,12 +279,12 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 if (r >= hs || !x0c) continue;
                 const int si = sidx(r);
                 const Off o = coef(r);
-                sr[r] -= pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, hN_x) +
+                sr[r] -= pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opN(pp, r, hN_x) +
                                             o.s * opS(pp, r, hS_x));     // x0c: hN_x/hS_x = x0 on the halo rows
             }
             if (hasS) {
                 const int si = sidx(-1);
-                hS_r0 = hS_bt - (x0c ? hS_x + hS_ci * (hS_o.e * op_s[si + 1] + hS_o.w * op_s[si - 1] +
+                hS_r0 = hS_bt - (x0c ? hS_x + hS_ci * (hS_o.e * op_s[si + dE] + hS_o.w * op_s[si + dW] +
                                                         hS_o.n * (hs > 0 ? pp[0] : 0.0) + hS_o.s * hS_x2)
                                      : 0.0);
             }
@@ -297,7 +295,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 // (a select chain, not pp[hs - 1]: a dynamic index would move pp to local memory for the whole kernel)
                 #pragma unroll
                 for (int r = 0; r < RMAX; ++r) xN = fma(r == hs - 1 ? 1.0 : 0.0, pp[r], xN);
-                hN_r0 = hN_bt - (x0c ? hN_x + hN_ci * (hN_o.e * op_s[si + 1] + hN_o.w * op_s[si - 1] +
+                hN_r0 = hN_bt - (x0c ? hN_x + hN_ci * (hN_o.e * op_s[si + dE] + hN_o.w * op_s[si + dW] +
                                                         hN_o.n * hN_x2 + hN_o.s * xN)
                                      : 0.0);
             }
@@ -317,7 +315,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 if (r >= hs) continue;
                 const int si = sidx(r);
                 const Off o = coef(r);
-                const double vv = pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(pp, r, hN_r0) +
+                const double vv = pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opN(pp, r, hN_r0) +
                                                      o.s * opS(pp, r, hS_r0));
                 v_s[r * BLOCK3 + tid] = vv;
                 a[3] += sr[r] * vv;
@@ -397,7 +395,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                         if (r >= hs) continue;
                         const int si = sidx(r);
                         const Off o = coef(r);
-                        const double vv = pp[r] + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] +
+                        const double vv = pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] +
                                                              o.n * opN(pp, r, haloN) + o.s * opS(pp, r, haloS));
                         v_s[r * BLOCK3 + tid] = vv;
                         a[0] += BT(r) * vv;
@@ -473,7 +471,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                         const int si = sidx(r);
                         const Off o = coef(r);
                         const double sv = sr[r];
-                        const double t = sv + cinv(r) * (o.e * op_s[si + 1] + o.w * op_s[si - 1] + o.n * opN(sr, r, haloN) +
+                        const double t = sv + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opN(sr, r, haloN) +
                                                          o.s * opS(sr, r, haloS));
                         t_s[r * BLOCK3 + tid] = t;
                         const double b0 = BT(r);

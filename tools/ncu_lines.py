@@ -1,5 +1,6 @@
 """Per-source-line warp-stall samples from an ncu report (needs -lineinfo + --import-source).
-usage: python tools/ncu_lines.py report.ncu-rep [topN] [function-substring]"""
+usage: python tools/ncu_lines.py report.ncu-rep [topN] [function-substring] [stall-column ...]
+With stall columns (e.g. stall_wait stall_barrier), lines are ranked by their sum and each column is shown."""
 import csv
 import io
 import subprocess
@@ -9,10 +10,12 @@ from collections import defaultdict
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 want = sys.argv[3] if len(sys.argv) > 3 else ""
+cols = sys.argv[4:] or ["Warp Stall Sampling (All Samples)"]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
-f, fn, si = None, "", None
-rows = defaultdict(float)
+f, fn, ix = None, "", None
+rows = defaultdict(lambda: [0.0] * len(cols))
+allrow = "Warp Stall Sampling (All Samples)"
 for r in csv.reader(io.StringIO(out)):
     if not r:
         continue
@@ -23,15 +26,20 @@ for r in csv.reader(io.StringIO(out)):
         fn = r[1]
         continue
     if r[0] == "Line No":
-        si = r.index("Warp Stall Sampling (All Samples)")
+        ix = [r.index(c) for c in cols]
         continue
     if want and want not in fn:
         continue
-    if si is not None and len(r) > si and r[0] and r[2] == "-":
+    if ix is not None and len(r) > max(ix) and r[0] and r[2] == "-":
         try:
-            rows[(f, int(r[0]), r[1][:100])] += float(r[si])
+            v = rows[(f, int(r[0]), r[1][:90])]
+            for j, i in enumerate(ix):
+                v[j] += float(r[i] or 0)
         except ValueError:
             pass
-tot = sum(rows.values()) or 1
-for (f, ln, src), v in sorted(rows.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"{100 * v / tot:5.1f}%  {f}:{ln}  {src}")
+tot = [sum(v[j] for v in rows.values()) or 1 for j in range(len(cols))]
+grand = sum(tot)
+for (f, ln, src), v in sorted(rows.items(), key=lambda kv: -sum(kv[1]))[:top]:
+    parts = "  ".join(f"{100 * v[j] / grand:5.1f}%" for j in range(len(cols)))
+    print(f"{parts}  {f}:{ln}  {src}")
+print("columns:", ", ".join(f"{c} {100 * t / grand:.1f}%" for c, t in zip(cols, tot)))
