@@ -754,6 +754,8 @@ int pit_residual_device(pit_handle* h, const double* d_U, const double* d_u0, co
 // Batch of independent level solves A_{lev[a]} x_a = b_a (A at the iterate d_U [nt][ns]); chunks of <= D.
 static int level_solves(pit_handle* h, int nb, const int* lev, const double* const* b, double* const* x, const double* d_U,
                         const double* d_bc, int* d_info, cudaStream_t st) {
+    if (h->engine == 3 && ((uintptr_t)d_U % 16) != 0)     // engine 3 stages u rows in 16-byte pieces
+        return set_err(h, PIT_EINVAL, "d_U must be 16-byte aligned");
     for (int a0 = 0; a0 < nb; a0 += h->D) {
         SolveParams S = base_params(h);
         S.U = const_cast<double*>(d_U);

@@ -130,31 +130,29 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         const bool x0c = S.x0carry && S.mode == 0 && n > 1;
         const bool hasS = hs > 0 && own_top && top_valid, hasN = hs > 0 && own_bot && bot_valid;
         double up[RMAX];
-        // stage u of the own column, rows -1 .. hs, with the E/W halo columns (periodic wrap or Dirichlet
-        // ring) written by the edge columns (cp.async for values inside the domain: all loads in flight)
-        auto stage_u = [&](int ui, int gr, int gc) {
-            bool inside = true;
-            if (P.bc == 1) {
-                gr = gr < 0 ? gr + nyu : (gr >= nyu ? gr - nyu : gr);
-                gc = gc < 0 ? gc + nxu : (gc >= nxu ? gc - nxu : gc);
-            } else {
-                inside = gr >= 0 && gr < nyu && gc >= 0 && gc < nxu;
-            }
-            if (inside) {
-                const unsigned dst = (unsigned)__cvta_generic_to_shared(u_s + ui);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(Ulev + (long long)gr * nxu + gc)
+        // stage u of the strip, rows -1 .. h, in 16-byte pieces (cp.async.cg: every thread copies column pairs of
+        // whole rows, independent of the column it owns; periodic rows wrap).  Dirichlet ring rows and the E/W halo
+        // columns (the ring) are written with ordinary stores.
+        {
+            const int lg = nxu == 512 ? 8 : 7, half = nxu >> 1;        // column pairs per row (nxu = 512 or 256)
+            const int npairs = (h > 0 ? h + 2 : 0) << lg;
+            for (int i = tid; i < npairs; i += BLOCK3) {
+                const int rr = (i >> lg) - 1, cpair = i & (half - 1);
+                int gr = r0 + rr;
+                if (P.bc == 1) gr = gr < 0 ? gr + nyu : (gr >= nyu ? gr - nyu : gr);
+                else if (gr < 0 || gr >= nyu) continue;
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(u_s + (rr + 1) * W + 2 + 2 * cpair);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(Ulev + (long long)gr * nxu + 2 * cpair)
                              : "memory");
-            } else {
-                u_s[ui] = node_ext(P, Ulev, ringn, gr, gc);
             }
-        };
-        #pragma unroll 1
-        for (int r = -1; r <= hs; ++r) {
-            if (hs == 0) break;
-            const int ui = uidx(r), gr = r0 + R0 + r;
-            stage_u(ui, gr, col);
-            if (P.bc != 1 && col == 0) stage_u(ui - 1, gr, -1);          // W halo column: the Dirichlet ring
-            if (P.bc != 1 && col == nxu - 1) stage_u(ui + 1, gr, nxu);   // E halo column
+            if (P.bc != 1 && hs > 0) {
+                for (int r = -1; r <= hs; ++r) {
+                    const int ui = uidx(r), gr = r0 + R0 + r;
+                    if (gr < 0 || gr >= nyu) u_s[ui] = node_ext(P, Ulev, ringn, gr, col);
+                    if (col == 0) u_s[ui - 1] = node_ext(P, Ulev, ringn, gr, -1);
+                    if (col == nxu - 1) u_s[ui + 1] = node_ext(P, Ulev, ringn, gr, nxu);
+                }
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         PMARK(12);
