@@ -41,6 +41,21 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     __shared__ double lacc[MAXD][4];                   // this CTA's norm partials per pipeline slot, summed over levels
     __shared__ double pro_s2, pro_mx, epi_s2, epi_mx;  // thread 0: this CTA's residual / update partials of the step
     __shared__ double prevmax_s;
+    // this CTA's share of a step with A active pairs (A = 1..MAXD), computed once: pair me, its CTA block [g0, g1),
+    // the strip rows [r0, r1) and the CTAs owning the halo rows r0 - 1 / r1 (integer divisions kept off the step path)
+    __shared__ int s_asg[MAXD + 1][8];
+    if (tid < MAXD) {
+        const int A = tid + 1;
+        int me = 0;
+        while (me + 1 < A && (me + 1) * G / A <= g) ++me;                 // 32-bit: G * A < 2^31
+        const int g0 = me * G / A, g1 = (me + 1) * G / A, C = g1 - g0, c = g - g0;
+        const int r0 = c * nyu / C, r1 = (c + 1) * nyu / C;                // 32-bit: C * nyu < 2^31
+        const int trow = r0 == 0 ? nyu - 1 : r0 - 1, brow = r1 == nyu ? 0 : r1;
+        int* t = s_asg[A];
+        t[0] = me; t[1] = g0; t[2] = g1; t[3] = r0; t[4] = r1;
+        t[5] = g0 + ((trow + 1) * C - 1) / nyu;                             // owner of row r0 - 1 in the pair
+        t[6] = g0 + ((brow + 1) * C - 1) / nyu;                             // owner of row r1
+    }
     if (tid == 0) {
         const int D = S.D;
         for (int k = 0; k < S.newton_max; ++k) {
@@ -81,33 +96,31 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         int A = 0;
         for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ks[A++] = k;
         if (S.mode == 1) { A = S.nb; for (int a = 0; a < A; ++a) ks[a] = a; }
-        int me = 0;
-        while (me + 1 < A && (me + 1) * G / A <= g) ++me;                 // 32-bit: G * A < 2^31
-        const int g0 = me * G / A, g1 = (me + 1) * G / A;
+        const int* const asg = s_asg[A];
+        const int me = asg[0], g0 = asg[1], g1 = asg[2];
         const int kme = ks[me];
         const int n = S.mode == 1 ? S.blev[me] : step - sS[kme] + 1;
         const int slot = kme % S.D;
         const int buf = kme % S.B, nbuf = (kme + 1) % S.B;
         const Slot sl = slot_at(S.slotmem, ns, slot);
         double* const pX = sl.x;
-        const int c = g - g0, C = g1 - g0;
-        const int r0 = c * nyu / C, r1 = (c + 1) * nyu / C;                // 32-bit: C * nyu < 2^31
+        const int c = g - g0;
+        const int r0 = asg[3], r1 = asg[4];
         const int h = r1 - r0;
         const double* Ulev = S.mode == 1 ? S.U + (long long)(n - 1) * ns : S.U + ((long long)buf * P.nt + (n - 1)) * ns;
         const double* uprev = n == 1 ? S.u0 : Ulev - ns;
         const double* ringn = S.ring ? S.ring + (long long)(n - 1) * P.ring_len : nullptr;
         double* Unew = S.mode == 1 ? nullptr : S.U + ((long long)nbuf * P.nt + (n - 1)) * ns;
         // this thread's sub-strip of rows [R0, R1) (strip-local), column col
-        const int R0 = grp * h / Gr, R1 = (grp + 1) * h / Gr;
+        const int R0 = (grp * h) >> (Gr - 1), R1 = ((grp + 1) * h) >> (Gr - 1);   // Gr = 1 or 2
         const int hs = R1 - R0;
         const bool own_top = R0 == 0, own_bot = R1 == h;          // sub-strip touches the CTA's halo rows
         const bool top_valid = P.bc == 1 || r0 > 0, bot_valid = P.bc == 1 || r1 < nyu;
-        const int top_row = r0 == 0 ? nyu - 1 : r0 - 1, bot_row = r1 == nyu ? 0 : r1;
         // published boundary rows: own {top, bottom} slots, and the bottom slot of the CTA owning row r0 - 1 /
         // the top slot of the CTA owning row r1 (owner of row x in the pair: ((x + 1) C - 1) / nyu)
         double* const hb_own = S.halo + (long long)g * HALO_CTA + col;
-        const double* const hb_S = S.halo + (long long)(g0 + ((top_row + 1) * C - 1) / nyu) * HALO_CTA + 6 * HALO_ROW + col;
-        const double* const hb_N = S.halo + (long long)(g0 + ((bot_row + 1) * C - 1) / nyu) * HALO_CTA + col;
+        const double* const hb_S = S.halo + (long long)asg[5] * HALO_CTA + 6 * HALO_ROW + col;
+        const double* const hb_N = S.halo + (long long)asg[6] * HALO_CTA + col;
         auto pub = [&](int R, int v, double val) {     // row R of the strip is a boundary row: publish
             if (R == 0) hb_own[v * HALO_ROW] = val;
             if (R == h - 1) hb_own[(6 + v) * HALO_ROW] = val;
