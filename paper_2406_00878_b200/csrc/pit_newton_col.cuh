@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     // this CTA's share of a step with A active pairs (A = 1..MAXD), computed once: pair me, its CTA block [g0, g1),
     // the strip rows [r0, r1) and the CTAs owning the halo rows r0 - 1 / r1 (integer divisions kept off the step path)
     __shared__ int s_asg[MAXD + 1][8];
+    __shared__ unsigned char s_kD[MAXK + 1], s_kB[MAXK + 1];   // k mod D (pipeline slot), k mod B (iterate buffer)
+    for (int k = tid; k <= MAXK; k += BLOCK3) { s_kD[k] = (unsigned char)(k % S.D); s_kB[k] = (unsigned char)(k % S.B); }
     if (tid < MAXD) {
         const int A = tid + 1;
         int me = 0;
@@ -100,8 +102,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         const int me = asg[0], g0 = asg[1], g1 = asg[2];
         const int kme = ks[me];
         const int n = S.mode == 1 ? S.blev[me] : step - sS[kme] + 1;
-        const int slot = kme % S.D;
-        const int buf = kme % S.B, nbuf = (kme + 1) % S.B;
+        const int slot = s_kD[kme];
+        const int buf = s_kB[kme], nbuf = s_kB[kme + 1];
         const Slot sl = slot_at(S.slotmem, ns, slot);
         double* const pX = sl.x;
         const int c = g - g0;
@@ -544,18 +546,18 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             for (int aa = 0; aa < A; ++aa)
                 if (step - sS[ks[aa]] + 1 == P.nt) kc = ks[aa];
         if (S.mode == 0 && tid == 0) {
-            const int so = kme % S.D;
+            const int so = s_kD[kme];
             lacc[so][0] += pro_s2; lacc[so][1] = fmax(lacc[so][1], pro_mx);
             lacc[so][2] += epi_s2; lacc[so][3] = fmax(lacc[so][3], epi_mx);
             if (kc >= 0) {
-                const int sa = kc % S.D;
+                const int sa = s_kD[kc];
                 double* hq = S.hpart + ((long long)sa * G + g) * 4;
                 for (int j = 0; j < 4; ++j) { hq[j] = lacc[sa][j]; lacc[sa][j] = 0.0; }
             }
         }
         if (kc >= 0) {
             bar_sync(S.bs, G, ep, false, hi);
-            const double* hq = S.hpart + (long long)(kc % S.D) * G * 4;
+            const double* hq = S.hpart + (long long)s_kD[kc] * G * 4;
             for (int j = tid; j < G * 4; j += BLOCK3) s_hp_big[j] = __ldcg(hq + j);
             __syncthreads();
             __shared__ int s_stop[3];                  // stop_status, stop_k, last_done (thread 0 -> all)
