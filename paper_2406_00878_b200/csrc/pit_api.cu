@@ -672,6 +672,10 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
     if (d_hist) CUDA_TRY(h, cudaMemsetAsync(d_hist, 0, sizeof(double) * 4 * h->cfg.newton_max, st));
     h->product_used = 0;
     if (want_product(h, d_bc, st)) return solve_product(h, d_u0, d_bc, d_u_out, d_hist, (int*)d_info, st);
+    if (((uintptr_t)d_u0 % 16) != 0) {         // engine 3 stages u^0 rows in 16-byte pieces
+        CUDA_TRY(h, cudaMemcpyAsync(h->d_u0, d_u0, sizeof(double) * h->P.ns, cudaMemcpyDeviceToDevice, st));
+        d_u0 = h->d_u0;
+    }
     SolveParams S = base_params(h);
     S.u0 = d_u0;
     S.ring = h->P.bc == PIT_DIRICHLET ? d_bc : nullptr;

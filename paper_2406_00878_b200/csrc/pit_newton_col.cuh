@@ -144,7 +144,6 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         // u (two rows deep), u^{n-1} and the carry, all of which are inputs of this step.
         const bool x0c = S.x0carry && S.mode == 0 && n > 1;
         const bool hasS = hs > 0 && own_top && top_valid, hasN = hs > 0 && own_bot && bot_valid;
-        double up[RMAX];
         // stage u of the strip, rows -1 .. h, in 16-byte pieces (cp.async.cg: every thread copies column pairs of
         // whole rows, independent of the column it owns; periodic rows wrap).  Dirichlet ring rows and the E/W halo
         // columns (the ring) are written with ordinary stores.
@@ -159,6 +158,23 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(u_s + (rr + 1) * W + 2 + 2 * cpair);
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(Ulev + (long long)gr * nxu + 2 * cpair)
                              : "memory");
+            }
+            // mode 0: the own rows of u^{n-1} -> t_s and of the carry du^{n-1} -> x_s (= x0), same 16-byte pieces,
+            // in the [row of the column group][thread] layout of the strip vectors
+            if (S.mode == 0 && h > 0) {
+                const bool cpx = n > 1;
+                const int nq = h << lg, hh = h >> 1;
+                for (int i = tid; i < nq; i += BLOCK3) {
+                    const int j = i >> lg, cpair = i & (half - 1);             // strip row j
+                    const int gsel = (Gr == 2 && j >= hh) ? 1 : 0;
+                    const int soff = (j - (gsel ? hh : 0)) * BLOCK3 + gsel * nxu + 2 * cpair;
+                    const long long q = (long long)(r0 + j) * nxu + 2 * cpair;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(t_s + soff)),
+                                 "l"(uprev + q) : "memory");
+                    if (cpx)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(x_s + soff)),
+                                     "l"(pX + q) : "memory");
+                }
             }
             if (P.bc != 1 && hs > 0) {
                 for (int r = -1; r <= hs; ++r) {
@@ -179,17 +195,9 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (S.mode == 1 || n == 1 || (P.bc != 1 && (gr < 0 || gr >= nyu))) return 0.0;
             return __ldcg(pX + rowq(gr));
         };
-        #pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-            up[r] = 0.0; sr[r] = 0.0;
-            if (r < hs) {
-                if (S.mode == 1) {
-                    sr[r] = __ldcg(S.bptr[me] + q_of(r));
-                } else {
-                    up[r] = __ldcg(uprev + q_of(r));
-                    sr[r] = n == 1 ? 0.0 : __ldcg(pX + q_of(r));
-                }
-            }
+        if (S.mode == 1) {
+            #pragma unroll
+            for (int r = 0; r < RMAX; ++r) sr[r] = r < hs ? __ldcg(S.bptr[me] + q_of(r)) : 0.0;
         }
         // halo-point inputs: S halo (row r0-1) and N halo (row r1) of this column
         double hS_u2 = 0.0, hS_up = 0.0, hS_x = 0.0, hS_x2 = 0.0, hS_b = 0.0;
@@ -211,6 +219,12 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         PMARK(7);
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
+        if (S.mode == 0) {
+            #pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+                sr[r] = (r < hs && n > 1) ? X(r) : 0.0;
+            }
+        }
         PMARK(8);
         // operand accessors: N/S from registers inside the sub-strip, shared memory across the column-group
         // boundary, the halo register across the CTA boundary; E/W from shared memory
@@ -242,7 +256,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 const int ui = uidx(r);
                 const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], u_s[ui - W]};
                 double G, aC;
-                res_diag<LAW>(P, v, up[r], G, aC);
+                res_diag<LAW>(P, v, S.mode == 0 ? t_s[r * BLOCK3 + tid] : 0.0, G, aC);   // u^{n-1} (staged)
                 double rhs;
                 if (S.mode == 1) {
                     rhs = sr[r];
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 const double ci = LAW == 1 ? ci_const : 1.0 / aC;
                 if (LAW != 1) ci_s[r * BLOCK3 + tid] = ci;
                 const double x0 = x0c ? sr[r] : 0.0;
-                X(r) = x0;
+                if (!x0c) X(r) = 0.0;                  // x0c: x_s already holds x0 = du^{n-1} (staged)
                 sr[r] = rhs * ci;                      // b~ (r0 once the x0 matvec is subtracted)
                 a[2] += sr[r] * sr[r];
                 pp[r] = x0;
