@@ -125,58 +125,56 @@ __device__ __forceinline__ bool bar_sync(BarState* b, unsigned G, unsigned& ep, 
     return s_any;
 }
 
-// bar_sync fused with the pair reduction: after thread 0's acquire, warp 0 loads the partials of CTAs [g0, g1)
-// straight from L2 (lane l sums CTAs g0 + l, g0 + l + 32, ... in order, then a fixed butterfly: the same order as
-// pair_reduce2) and the barrier's closing __syncthreads broadcasts them.  Two CTA barriers per grid barrier.
+// bar_sync fused with the pair reduction: after thread 0's acquire, warps 0..N-1 each reduce one of the N values
+// over the pair's CTAs [g0, g1): lane l loads the partials of CTAs g0 + l, g0 + l + 32, ... (all loads issued
+// together: one L2 round trip) and sums them in that order, then a fixed butterfly — the same order for every
+// value as a single-warp loop, so results are bit-identical run to run.  C = g1 - g0 <= GMAX2 = 160.
 template <int NS, int NM>
 __device__ __forceinline__ bool bar_sync_reduce(BarState* b, unsigned G, unsigned& ep, bool flag, unsigned (&hi)[2],
                                                 const double* part, int stride, int g0, int g1, double (&out)[NS + NM],
                                                 double* sm) {
     constexpr int N = NS + NM;
+    constexpr int J = GMAX2 / 32;
     __shared__ unsigned s_any2;
     __syncthreads();
-    if ((threadIdx.x >> 5) == 0) {
-        if (threadIdx.x == 0) {
-            unsigned long long* ctr = b->ctr + 16 * (ep & 1);
-            const unsigned long long add = 1ull | ((unsigned long long)(flag ? 1u : 0u) << 32);
-            asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(add) : "memory");
-            const unsigned target = (ep / 2 + 1) * G;
-            unsigned long long v;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-            } while ((unsigned)v < target);
-            const unsigned h = (unsigned)(v >> 32);
-            s_any2 = h != hi[ep & 1];
-            hi[ep & 1] = h;
-        }
-        __syncwarp();
-        double a[N];
-        #pragma unroll
-        for (int i = 0; i < N; ++i) a[i] = 0.0;
-        for (int t = g0 + (int)threadIdx.x; t < g1; t += 32) {
-            const double* pg = part + (long long)t * stride;
-            #pragma unroll
-            for (int i = 0; i < N; ++i) {
-                const double y = __ldcg(pg + i);
-                a[i] = i < NS ? a[i] + y : fmax(a[i], y);
-            }
-        }
-        #pragma unroll
-        for (int i = 0; i < N; ++i)
-            #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double y = __shfl_xor_sync(0xffffffffu, a[i], o);
-                a[i] = i < NS ? a[i] + y : fmax(a[i], y);
-            }
-        if (threadIdx.x == 0)
-            #pragma unroll
-            for (int i = 0; i < N; ++i) sm[i] = a[i];
+    if (threadIdx.x == 0) {
+        unsigned long long* ctr = b->ctr + 16 * (ep & 1);
+        const unsigned long long add = 1ull | ((unsigned long long)(flag ? 1u : 0u) << 32);
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(add) : "memory");
+        const unsigned target = (ep / 2 + 1) * G;
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        } while ((unsigned)v < target);
+        const unsigned h = (unsigned)(v >> 32);
+        s_any2 = h != hi[ep & 1];
+        hi[ep & 1] = h;
     }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (w < N) {                                        // a warp-uniform condition
+        double y[J];
+        #pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int t = g0 + l + 32 * j;
+            y[j] = t < g1 ? __ldcg(part + (long long)t * stride + w) : 0.0;
+        }
+        double a = 0.0;
+        #pragma unroll
+        for (int j = 0; j < J; ++j) a = w < NS ? a + y[j] : fmax(a, y[j]);
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double z = __shfl_xor_sync(0xffffffffu, a, o);
+            a = w < NS ? a + z : fmax(a, z);
+        }
+        if (l == 0) sm[w] = a;
+    }
+    const bool any = s_any2;
     ++ep;
     __syncthreads();
     #pragma unroll
     for (int i = 0; i < N; ++i) out[i] = sm[i];
-    return s_any2;
+    return any;
 }
 
 // u at unknown (gc, gr) of level n, extended by the Dirichlet ring (Eq. 2) or the periodic wrap.
