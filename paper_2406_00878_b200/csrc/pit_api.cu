@@ -185,15 +185,20 @@ static const void* onchip_fn_t(int ppt) {
     }
 }
 
-template <bool TR, int LAW>
+template <bool TR, int LAW, int NXU>
 static const void* col_fn_t(int rmax) {
-    return rmax <= 4 ? (const void*)k_newton_col<4, TR, LAW>
-                     : (rmax <= 7 ? (const void*)k_newton_col<7, TR, LAW> : (const void*)k_newton_col<8, TR, LAW>);
+    return rmax <= 4 ? (const void*)k_newton_col<4, TR, LAW, NXU>
+                     : (rmax <= 7 ? (const void*)k_newton_col<7, TR, LAW, NXU> : (const void*)k_newton_col<8, TR, LAW, NXU>);
 }
 
-static const void* col_fn(int rmax, bool trace, int law) {
-    if (law == 1) return trace ? col_fn_t<true, 1>(rmax) : col_fn_t<false, 1>(rmax);
-    return trace ? col_fn_t<true, 0>(rmax) : col_fn_t<false, 0>(rmax);
+template <int NXU>
+static const void* col_fn_n(int rmax, bool trace, int law) {
+    if (law == 1) return trace ? col_fn_t<true, 1, NXU>(rmax) : col_fn_t<false, 1, NXU>(rmax);
+    return trace ? col_fn_t<true, 0, NXU>(rmax) : col_fn_t<false, 0, NXU>(rmax);
+}
+
+static const void* col_fn(int rmax, bool trace, int law, int nxu) {
+    return nxu == 512 ? col_fn_n<512>(rmax, trace, law) : col_fn_n<256>(rmax, trace, law);
 }
 
 // LAW 1 = viscous Burgers with constant viscosity (m2 = 0): specialised matvec coefficients.
@@ -301,7 +306,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
             bool ok = true;
             int occ3 = 0;
             for (bool tr : {false, true}) {
-                const void* fn = col_fn(rmax, tr, law);
+                const void* fn = col_fn(rmax, tr, law, P.nxu);
                 ok = ok && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
                      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, fn, BLOCK3, smem) == cudaSuccess && occ3 >= 1;
             }
@@ -369,7 +374,7 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
         (rc = dalloc(h, &h->d_small, 2 * 1024 + 2)) ||
         (rc = dalloc(h, &h->bs, 1)) ||
-        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 13)))) {
+        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 13 + 13 * GMAX2)))) {
         free_all(h);
         delete h;
         return rc;
@@ -480,7 +485,7 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
         CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
         // the dynamic shared-memory limit is a per-function attribute shared by every handle of the process
         // (e.g. the nested coarse-grid handle): set it for this launch
-        const void* fn = h->engine == 3 ? col_fn(h->ppt, h->trace != nullptr, h->law) : onchip_fn(h->ppt, h->trace != nullptr, h->law);
+        const void* fn = h->engine == 3 ? col_fn(h->ppt, h->trace != nullptr, h->law, h->P.nxu) : onchip_fn(h->ppt, h->trace != nullptr, h->law);
         CUDA_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem2));
         CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->G), dim3(h->engine == 3 ? BLOCK3 : BLOCK2), args, h->smem2, st));
     } else {
@@ -921,6 +926,13 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
         float t_guess = 0.f;
         if (h->guess_timed) CUDA_TRY(h, cudaEventElapsedTime(&t_guess, h->ev[4], h->ev[5]));
         out[17 + MAXK + 6] = (long long)(t_guess * 1e6);
+    }
+    // trace builds: per-CTA cycle accounts [G][13] after the fixed fields (engine 3 only; tools/skew_run.py)
+    const int base = 17 + MAXK + 7;
+    if (h->trace && h->engine == 3 && n >= base + 13 * h->G) {
+        std::vector<unsigned long long> pc((size_t)13 * h->G);
+        CUDA_TRY(h, cudaMemcpy(pc.data(), h->trace + 13, pc.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < pc.size(); ++i) out[base + i] = (long long)pc[i];
     }
     return PIT_OK;
 }

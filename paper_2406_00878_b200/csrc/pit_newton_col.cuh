@@ -18,14 +18,18 @@ constexpr int HALO_ROW = 512;                          // doubles per published 
 constexpr int HALO_CTA = 2 * 6 * HALO_ROW;             // per CTA: {top, bottom} x {s, t, p, v, r, v2}
 enum { HV_S = 0, HV_T = 1, HV_P = 2, HV_V = 3, HV_R = 4, HV_V2 = 5 };
 
-template <int RMAX, bool TRACE, int LAW>
+// NXU (unknowns per row, 256 or 512) is a template parameter: the row pitch W and the column-group split are then
+// compile-time constants, so every shared-memory offset of the stencil loops folds into an immediate (with a
+// runtime pitch the 128-register budget forced the compiler to rematerialise the index arithmetic in every loop).
+template <int RMAX, bool TRACE, int LAW, int NXU>
 __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     extern __shared__ double smem[];
     const Prob P = S.P;
     const long long ns = P.ns;
-    const int nxu = P.nxu, nyu = P.nyu;
+    constexpr int nxu = NXU;
+    const int nyu = P.nyu;
     const int G = S.G, g = blockIdx.x, tid = threadIdx.x;
-    const int W = nxu + 4;                             // row pitch of u_s / op_s: data at +2 (16-byte aligned rows)
+    constexpr int W = nxu + 4;                         // row pitch of u_s / op_s: data at +2 (16-byte aligned rows)
     const int HM = S.hmax;
     double* const u_s = smem;                          // [HM+2][W] u of the strip rows + halo rows (+ ring / wrap columns)
     double* const op_s = u_s + (HM + 2) * W;           // [HM+2][W] matvec operand (E/W exchange, halo rows)
@@ -77,14 +81,17 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     long long t_last = clock64();
     auto flush_prof = [&]() {
         if (TRACE && tid == 0)
-            for (int j = 0; j < 13; ++j) atomicAdd(S.trace + j, (unsigned long long)prof[j]);
+            for (int j = 0; j < 13; ++j) {
+                atomicAdd(S.trace + j, (unsigned long long)prof[j]);
+                S.trace[13 + 13 * g + j] = (unsigned long long)prof[j];    // per-CTA copy (tools/skew_run.py)
+            }
     };
     const int newton_max = S.mode == 0 ? S.newton_max : 1;
     int set = 0, klo = 0, last_done = -1;
     long long total_inner = 0;
     const double rtol2 = S.lin_rtol * S.lin_rtol;
     const double atol2 = S.lin_atol * S.lin_atol * (double)P.ns;     // lin_atol bounds the RMS residual
-    const int Gr = BLOCK3 / nxu;                       // column groups (1 or 2)
+    constexpr int Gr = BLOCK3 / nxu;                   // column groups (1 or 2)
     const int col = tid % nxu, grp = tid / nxu;
     // E / W neighbours in the u_s / op_s rows: the next column, or the periodic wrap inside the row; Dirichlet
     // edges read the halo columns (u_s: the ring, staged every step; op_s: zeros, written once below)
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         // whole rows, independent of the column it owns; periodic rows wrap).  Dirichlet ring rows and the E/W halo
         // columns (the ring) are written with ordinary stores.
         {
-            const int lg = nxu == 512 ? 8 : 7, half = nxu >> 1;        // column pairs per row (nxu = 512 or 256)
+            constexpr int lg = nxu == 512 ? 8 : 7, half = nxu >> 1;    // column pairs per row (nxu = 512 or 256)
             const int npairs = (h > 0 ? h + 2 : 0) << lg;
             for (int i = tid; i < npairs; i += BLOCK3) {
                 const int rr = (i >> lg) - 1, cpair = i & (half - 1);
