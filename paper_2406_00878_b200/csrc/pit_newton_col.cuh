@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     const double rtol2 = S.lin_rtol * S.lin_rtol;
     const double atol2 = S.lin_atol * S.lin_atol * (double)P.ns;     // lin_atol bounds the RMS residual
     constexpr int Gr = BLOCK3 / nxu;                   // column groups (1 or 2)
-    const int col = tid % nxu, grp = tid / nxu;
+    const int col = Gr == 1 ? tid : tid % nxu, grp = Gr == 1 ? 0 : tid / nxu;   // Gr = 1: R0 = 0 at compile time
     // E / W neighbours in the u_s / op_s rows: the next column, or the periodic wrap inside the row; Dirichlet
     // edges read the halo columns (u_s: the ring, staged every step; op_s: zeros, written once below)
     const int dE = (P.bc == 1 && col == nxu - 1) ? -(nxu - 1) : 1;

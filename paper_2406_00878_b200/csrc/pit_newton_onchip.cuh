@@ -29,6 +29,47 @@ __device__ __forceinline__ void block_reduce2(double (&a)[NS + NM], double* sm) 
     // butterfly inside each warp, then warp 0 combines the NWARP2 per-warp values with a second (fixed)
     // butterfly: no serial loop over warps.  Result valid in thread 0.
     constexpr int N = NS + NM;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    auto op = [](int vi, double x, double y) { return vi < NS ? x + y : fmax(x, y); };
+    if constexpr (N >= 4 && N <= 8 && NWARP2 == 16) {
+        // transposed butterfly: every exchange halves the values a lane carries (padded to 8 with 0, which is
+        // neutral for the sums and for the maxima of non-negative values): 4 + 2 + 1 + 1 + 1 shuffles instead
+        // of 5 N; lane l ends with value 4 b4 + 2 b3 + b2 (b = bits of l) reduced over the warp
+        const int h4 = (l >> 4) & 1, h3 = (l >> 3) & 1, h2 = (l >> 2) & 1;
+        double c[4];
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double lo = j < N ? a[j] : 0.0, hi = j + 4 < N ? a[j + 4] : 0.0;
+            c[j] = op(4 * h4 + j, h4 ? hi : lo, __shfl_xor_sync(0xffffffffu, h4 ? lo : hi, 16));
+        }
+        double d[2];
+        #pragma unroll
+        for (int j = 0; j < 2; ++j)
+            d[j] = op(4 * h4 + 2 * h3 + j, h3 ? c[j + 2] : c[j], __shfl_xor_sync(0xffffffffu, h3 ? c[j] : c[j + 2], 8));
+        const int vi = 4 * h4 + 2 * h3 + h2;
+        double e = op(vi, h2 ? d[1] : d[0], __shfl_xor_sync(0xffffffffu, h2 ? d[0] : d[1], 4));
+        e = op(vi, e, __shfl_xor_sync(0xffffffffu, e, 2));
+        e = op(vi, e, __shfl_xor_sync(0xffffffffu, e, 1));
+        if ((l & 3) == 0 && vi < N) sm[w * N + vi] = e;
+        __syncthreads();
+        if (w == 0) {
+            // lane l: value i = l / 4 over warps l % 4, + 4, + 8, + 12 in that order, then a 4-lane butterfly;
+            // value i ends in lane 4 i and is broadcast to the warp
+            const int i = l >> 2, q = l & 3;
+            double v = 0.0;
+            if (i < N) {
+                v = sm[q * N + i];
+                #pragma unroll
+                for (int m = 1; m < 4; ++m) v = op(i, v, sm[(q + 4 * m) * N + i]);
+            }
+            v = op(i, v, __shfl_xor_sync(0xffffffffu, v, 2));
+            v = op(i, v, __shfl_xor_sync(0xffffffffu, v, 1));
+            #pragma unroll
+            for (int ii = 0; ii < N; ++ii) a[ii] = __shfl_sync(0xffffffffu, v, 4 * ii);
+        }
+        if (BCAST) __syncthreads();
+        return;
+    }
     #pragma unroll
     for (int i = 0; i < N; ++i)
         #pragma unroll
@@ -36,7 +77,6 @@ __device__ __forceinline__ void block_reduce2(double (&a)[NS + NM], double* sm) 
             const double y = __shfl_xor_sync(0xffffffffu, a[i], o);
             a[i] = i < NS ? a[i] + y : fmax(a[i], y);
         }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     if (l == 0)
         #pragma unroll
         for (int i = 0; i < N; ++i) sm[w * N + i] = a[i];
