@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round measurement bundle (run on the GPU box from the repo root): bench lines, launch list, ncu captures.
 set -u
-OUT=gpurun_out/round
+OUT=${1:-gpurun_out/round}
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > $OUT/gpu.txt 2>&1
 python bench.py > $OUT/bench_c5.json 2> $OUT/bench_c5.err
