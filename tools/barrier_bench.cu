@@ -1,0 +1,79 @@
+// barrier_bench.cu — the engine-3 barrier + pair reduction in isolation (148 CTAs x 512 threads, 2 pairs, 5 partials
+// per CTA), in variants of the spin:
+//   0: red.release arrival, ld.acquire spin, partial loads after the barrier (what k_newton_col does)
+//   1: red.release arrival, ld.relaxed spin + fence.acq_rel.gpu after it
+//   2: variant 0 with __nanosleep(32) between polls
+//   3: variant 0 without the partial loads (barrier only)
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o barrier_bench barrier_bench.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+
+template <int V>
+__global__ void __launch_bounds__(512, 1) bench(unsigned long long* ctr, double* part, int iters, double* out) {
+    __shared__ double sm[8];
+    const int G = gridDim.x, g = blockIdx.x, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int g0 = g < G / 2 ? 0 : G / 2, g1 = g < G / 2 ? G / 2 : G;
+    double acc = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        double* pset = part + (size_t)(it & 1) * G * 8;
+        if (threadIdx.x < 5) pset[g * 8 + threadIdx.x] = acc + threadIdx.x + it;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long* c = ctr + 16 * (it & 1);
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(c) : "memory");
+            const unsigned long long target = (unsigned long long)(it / 2 + 1) * G;
+            unsigned long long v;
+            if (V == 1) {
+                do { asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory"); } while (v < target);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            } else {
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+                    if (v >= target) break;
+                    if (V == 2) __nanosleep(32);
+                }
+            }
+        }
+        __syncthreads();
+        if (V != 3 && w < 5) {
+            double y[5];
+            #pragma unroll
+            for (int j = 0; j < 5; ++j) { const int t = g0 + l + 32 * j; y[j] = t < g1 ? __ldcg(pset + t * 8 + w) : 0.0; }
+            double a = y[0] + y[1] + y[2] + y[3] + y[4];
+            #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (l == 0) sm[w] = a;
+        }
+        __syncthreads();
+        acc += V != 3 ? sm[0] * 1e-30 : 0.0;
+    }
+    if (acc == 1234.5) out[0] = acc;
+}
+
+template <int V>
+float run(int G, unsigned long long* ctr, double* part, double* out, int iters) {
+    cudaMemset(ctr, 0, 256);
+    void* args[] = {&ctr, &part, &iters, &out};
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    cudaLaunchCooperativeKernel((void*)bench<V>, G, 512, args, 0, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+    return ms;
+}
+
+int main() {
+    cudaDeviceProp pr; cudaGetDeviceProperties(&pr, 0);
+    const int G = pr.multiProcessorCount, iters = 20000;
+    unsigned long long* ctr; double *part, *out;
+    cudaMalloc(&ctr, 256); cudaMalloc(&part, 2 * G * 8 * sizeof(double)); cudaMalloc(&out, 8);
+    for (int rep = 0; rep < 2; ++rep) {
+        printf("G=%d: v0 acquire spin + partials %.3f us | v1 relaxed spin + fence %.3f us | v2 nanosleep %.3f us | v3 barrier only %.3f us\n", G,
+               1e3 * run<0>(G, ctr, part, out, iters) / iters, 1e3 * run<1>(G, ctr, part, out, iters) / iters,
+               1e3 * run<2>(G, ctr, part, out, iters) / iters, 1e3 * run<3>(G, ctr, part, out, iters) / iters);
+    }
+    return 0;
+}
