@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     }
                 }
                 if (do_epi) epi_done = true;
-                PMARK(1);
+                if (do_epi) PMARK(3); else PMARK(1);           // trace: epilogue slot vs phase-1 work
                 double o1[1];
                 const bool any = bar_sync_reduce<1, 0>(S.bs, G, ep, !conv, hi, S.part + (long long)set * G * NPART, NPART,
                                                        g0, g1, o1, s_red);
