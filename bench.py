@@ -153,6 +153,22 @@ def run_reference(args):
     return 0
 
 
+# Grid barrier + pair reduction on B200, measured in isolation (tools/barrier_bench.cu, profiles/r01d/barrier_bench.txt)
+BARRIER_US = 1.99
+
+
+def sync_floor(st, nit, t_newton):
+    """The latency floor of the persistent on-chip engines: a wavefront step with i BiCGSTAB iterations costs
+    2 i + 1 grid barriers, plus one norm barrier per Newton iteration; at the isolated barrier
+    cost that many barriers take `ms` of the solve's `t_newton`."""
+    if st.get("engine", 0) < 2:
+        return None
+    n = 2 * st["inner_iterations"] + st["steps"] + nit
+    ms = n * BARRIER_US * 1e-3
+    return {"grid_barriers": n, "us_each_isolated": BARRIER_US, "ms": ms, "frac_of_solve": ms / (t_newton * 1e3),
+            "source": "tools/barrier_bench.cu (profiles/r01d/barrier_bench.txt)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -295,6 +311,7 @@ def main():
                      "algorithmic": f"{BYTES_PER_DOF_IT} B per DOF per Newton iteration (SURVEY 8(d) fused minimum)"},
         "kernels": {"k_newton_ms": t_newton * 1e3, "wavefront_steps": st["steps"],
                     "bicgstab_iterations": st["inner_iterations"],
+                    "sync_floor": sync_floor(st, nit, t_newton),
                     "k_resjac": {"ms": resjac_ms, "GB/s": resjac_gbs, "frac": resjac_gbs / peak, "traffic": traffic_a,
                                  "algorithmic": f"{RESJAC_BYTES_PER_DOF} B/DOF",
                                  "kernel": "k_resjac_bulk (TMA-staged kernel a, all levels)"}},
