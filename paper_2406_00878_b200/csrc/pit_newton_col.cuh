@@ -21,6 +21,8 @@ enum { HV_S = 0, HV_T = 1, HV_P = 2, HV_V = 3, HV_R = 4, HV_V2 = 5 };
 // NXU (unknowns per row, 256 or 512) is a template parameter: the row pitch W and the column-group split are then
 // compile-time constants, so every shared-memory offset of the stencil loops folds into an immediate (with a
 // runtime pitch the 128-register budget forced the compiler to rematerialise the index arithmetic in every loop).
+template <int V> struct IC { static constexpr int value = V; };   // compile-time strip height tag (0 = run time)
+
 template <int RMAX, bool TRACE, int LAW, int NXU>
 __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     extern __shared__ double smem[];
@@ -243,6 +245,18 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (r > 0) return o[r - 1];
             return own_top ? haloS : op_s[sidx(r) - W];
         };
+        auto opNh = [&](const double (&o)[RMAX], int r, double haloN, int H) -> double {   // opN for H = hs
+            if (r + 1 < H) return o[r + 1];
+            return own_bot ? haloN : op_s[sidx(r) + W];
+        };
+        // the hot loops run with the strip height as a compile-time constant when it is RMAX or RMAX - 1 (every CTA
+        // of a pair differs by at most one row); the guards of the unrolled loops then fold away.  Only with one
+        // column group is hs CTA-uniform (the bodies contain __syncthreads), else it stays a run-time value.
+        auto with_hs = [&](auto&& body) {
+            if (Gr == 1 && hs == RMAX) body(IC<RMAX>{});
+            else if (Gr == 1 && hs == RMAX - 1) body(IC<RMAX - 1>{});
+            else body(IC<0>{});
+        };
         auto put_op_at = [&](int si, double val) {
             op_s[si] = val;
         };
@@ -256,106 +270,110 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         double hS_r0 = 0.0, hN_r0 = 0.0;       // r0 = p0 on the halo rows
         {
             double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // sum r0^2, sum r^2, sum b~^2, sum r0 v0 | max |r|
-            #pragma unroll
-            for (int r = 0; r < RMAX; ++r) {
-                pp[r] = 0.0;
-                if (r >= hs) continue;
-                const int ui = uidx(r);
-                const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], u_s[ui - W]};
-                double G, aC;
-                res_diag<LAW>(P, v, S.mode == 0 ? t_s[r * BLOCK3 + tid] : 0.0, G, aC);   // u^{n-1} (staged)
-                double rhs;
-                if (S.mode == 1) {
-                    rhs = sr[r];
-                } else {
-                    const double res = -G;
-                    a[1] += res * res;
-                    a[4] = fmax(a[4], fabs(res));
-                    rhs = res + sr[r];                 // r^n + du^{n-1}  (row n of Eq. 7)
+            with_hs([&](auto tag) {
+                constexpr int HC = decltype(tag)::value;
+                const int H = HC ? HC : hs, HH = (HC && Gr == 1) ? HC : h;
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    pp[r] = 0.0;
+                    if (r >= H) continue;
+                    const int ui = uidx(r);
+                    const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], u_s[ui - W]};
+                    double G, aC;
+                    res_diag<LAW>(P, v, S.mode == 0 ? t_s[r * BLOCK3 + tid] : 0.0, G, aC);   // u^{n-1} (staged)
+                    double rhs;
+                    if (S.mode == 1) {
+                        rhs = sr[r];
+                    } else {
+                        const double res = -G;
+                        a[1] += res * res;
+                        a[4] = fmax(a[4], fabs(res));
+                        rhs = res + sr[r];                 // r^n + du^{n-1}  (row n of Eq. 7)
+                    }
+                    const double ci = LAW == 1 ? ci_const : 1.0 / aC;
+                    if (LAW != 1) ci_s[r * BLOCK3 + tid] = ci;
+                    const double x0 = x0c ? sr[r] : 0.0;
+                    if (!x0c) X(r) = 0.0;                  // x0c: x_s already holds x0 = du^{n-1} (staged)
+                    sr[r] = rhs * ci;                      // b~ (r0 once the x0 matvec is subtracted)
+                    a[2] += sr[r] * sr[r];
+                    pp[r] = x0;
+                    put_op(r, x0);
                 }
-                const double ci = LAW == 1 ? ci_const : 1.0 / aC;
-                if (LAW != 1) ci_s[r * BLOCK3 + tid] = ci;
-                const double x0 = x0c ? sr[r] : 0.0;
-                if (!x0c) X(r) = 0.0;                  // x0c: x_s already holds x0 = du^{n-1} (staged)
-                sr[r] = rhs * ci;                      // b~ (r0 once the x0 matvec is subtracted)
-                a[2] += sr[r] * sr[r];
-                pp[r] = x0;
-                put_op(r, x0);
-            }
-            // b~ - diag part on the halo points (u stencil: own column rows from u_s, the far row in a register)
-            double hS_ci = 0.0, hN_ci = 0.0, hS_bt = 0.0, hN_bt = 0.0;
-            Off hS_o = {0.0, 0.0, 0.0, 0.0}, hN_o = {0.0, 0.0, 0.0, 0.0};
-            if (hasS) {
-                const int ui = uidx(-1);
-                const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], hS_u2};
-                double G, aC;
-                res_diag<LAW>(P, v, hS_up, G, aC);
-                hS_ci = LAW == 1 ? ci_const : 1.0 / aC;
-                hS_bt = ((S.mode == 1 ? hS_b : -G + (n == 1 ? 0.0 : hS_x))) * hS_ci;
-                hS_o = offdiag_law<LAW>(P, v);
-                put_op_at(sidx(-1), x0c ? hS_x : 0.0);
-            }
-            if (hasN) {
-                const int ui = uidx(hs);
-                const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], hN_u2, u_s[ui - W]};
-                double G, aC;
-                res_diag<LAW>(P, v, hN_up, G, aC);
-                hN_ci = LAW == 1 ? ci_const : 1.0 / aC;
-                hN_bt = ((S.mode == 1 ? hN_b : -G + (n == 1 ? 0.0 : hN_x))) * hN_ci;
-                hN_o = offdiag_law<LAW>(P, v);
-                put_op_at(sidx(hs), x0c ? hN_x : 0.0);
-            }
-            PMARK(9);
-            __syncthreads();                           // op_s holds x0 on own rows + halo rows
-            // r0 = b~ - A~ x0 on own points and on the halo points
-            #pragma unroll
-            for (int r = 0; r < RMAX; ++r) {
-                if (r >= hs || !x0c) continue;
-                const int si = sidx(r);
-                const Off o = coef(r);
-                sr[r] -= pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opN(pp, r, hN_x) +
-                                            o.s * opS(pp, r, hS_x));     // x0c: hN_x/hS_x = x0 on the halo rows
-            }
-            if (hasS) {
-                const int si = sidx(-1);
-                hS_r0 = hS_bt - (x0c ? hS_x + hS_ci * (hS_o.e * op_s[si + dE] + hS_o.w * op_s[si + dW] +
-                                                        hS_o.n * (hs > 0 ? pp[0] : 0.0) + hS_o.s * hS_x2)
-                                     : 0.0);
-            }
-            if (hasN) {
-                const int si = sidx(hs);
-                double xN = 0.0;                       // x0 at the last own row (the halo point's S neighbour)
+                // b~ - diag part on the halo points (u stencil: own column rows from u_s, the far row in a register)
+                double hS_ci = 0.0, hN_ci = 0.0, hS_bt = 0.0, hN_bt = 0.0;
+                Off hS_o = {0.0, 0.0, 0.0, 0.0}, hN_o = {0.0, 0.0, 0.0, 0.0};
+                if (hasS) {
+                    const int ui = uidx(-1);
+                    const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], u_s[ui + W], hS_u2};
+                    double G, aC;
+                    res_diag<LAW>(P, v, hS_up, G, aC);
+                    hS_ci = LAW == 1 ? ci_const : 1.0 / aC;
+                    hS_bt = ((S.mode == 1 ? hS_b : -G + (n == 1 ? 0.0 : hS_x))) * hS_ci;
+                    hS_o = offdiag_law<LAW>(P, v);
+                    put_op_at(sidx(-1), x0c ? hS_x : 0.0);
+                }
+                if (hasN) {
+                    const int ui = uidx(H);
+                    const Vals v = {u_s[ui], u_s[ui + dE], u_s[ui + dW], hN_u2, u_s[ui - W]};
+                    double G, aC;
+                    res_diag<LAW>(P, v, hN_up, G, aC);
+                    hN_ci = LAW == 1 ? ci_const : 1.0 / aC;
+                    hN_bt = ((S.mode == 1 ? hN_b : -G + (n == 1 ? 0.0 : hN_x))) * hN_ci;
+                    hN_o = offdiag_law<LAW>(P, v);
+                    put_op_at(sidx(H), x0c ? hN_x : 0.0);
+                }
+                PMARK(9);
+                __syncthreads();                           // op_s holds x0 on own rows + halo rows
+                // r0 = b~ - A~ x0 on own points and on the halo points
                 #pragma unroll
-                // (a select chain, not pp[hs - 1]: a dynamic index would move pp to local memory for the whole kernel)
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= H || !x0c) continue;
+                    const int si = sidx(r);
+                    const Off o = coef(r);
+                    sr[r] -= pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opNh(pp, r, hN_x, H) +
+                                                o.s * opS(pp, r, hS_x));     // x0c: hN_x/hS_x = x0 on the halo rows
+                }
+                if (hasS) {
+                    const int si = sidx(-1);
+                    hS_r0 = hS_bt - (x0c ? hS_x + hS_ci * (hS_o.e * op_s[si + dE] + hS_o.w * op_s[si + dW] +
+                                                            hS_o.n * (H > 0 ? pp[0] : 0.0) + hS_o.s * hS_x2)
+                                         : 0.0);
+                }
+                if (hasN) {
+                    const int si = sidx(H);
+                    double xN = 0.0;                       // x0 at the last own row (the halo point's S neighbour)
+                    #pragma unroll
+                    // (a select chain, not pp[hs - 1]: a dynamic index would move pp to local memory for the whole kernel)
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) xN = fma(r == H - 1 ? 1.0 : 0.0, pp[r], xN);
+                    hN_r0 = hN_bt - (x0c ? hN_x + hN_ci * (hN_o.e * op_s[si + dE] + hN_o.w * op_s[si + dW] +
+                                                            hN_o.n * hN_x2 + hN_o.s * xN)
+                                         : 0.0);
+                }
+                __syncthreads();                           // all reads of x0 done: op_s <- p0 = r0
                 #pragma unroll
-                for (int r = 0; r < RMAX; ++r) xN = fma(r == hs - 1 ? 1.0 : 0.0, pp[r], xN);
-                hN_r0 = hN_bt - (x0c ? hN_x + hN_ci * (hN_o.e * op_s[si + dE] + hN_o.w * op_s[si + dW] +
-                                                        hN_o.n * hN_x2 + hN_o.s * xN)
-                                     : 0.0);
-            }
-            __syncthreads();                           // all reads of x0 done: op_s <- p0 = r0
-            #pragma unroll
-            for (int r = 0; r < RMAX; ++r) {
-                if (r >= hs) continue;
-                BT(r) = sr[r];                         // r0, and the BiCGSTAB shadow vector r^0 = r0
-                pp[r] = sr[r];                         // p0 = r0
-                a[0] += sr[r] * sr[r];
-                put_op(r, sr[r]);
-            }
-            __syncthreads();
-            // v0 = A~ p0; publish r0, v0 of the boundary rows (the halo of phase 2)
-            #pragma unroll
-            for (int r = 0; r < RMAX; ++r) {
-                if (r >= hs) continue;
-                const int si = sidx(r);
-                const Off o = coef(r);
-                const double vv = pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opN(pp, r, hN_r0) +
-                                                     o.s * opS(pp, r, hS_r0));
-                v_s[r * BLOCK3 + tid] = vv;
-                a[3] += sr[r] * vv;
-                const int R = R0 + r;
-                if (R == 0 || R == h - 1) { pub(R, HV_R, sr[r]); pub(R, HV_V2, vv); }
-            }
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= H) continue;
+                    BT(r) = sr[r];                         // r0, and the BiCGSTAB shadow vector r^0 = r0
+                    pp[r] = sr[r];                         // p0 = r0
+                    a[0] += sr[r] * sr[r];
+                    put_op(r, sr[r]);
+                }
+                __syncthreads();
+                // v0 = A~ p0; publish r0, v0 of the boundary rows (the halo of phase 2)
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= H) continue;
+                    const int si = sidx(r);
+                    const Off o = coef(r);
+                    const double vv = pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opNh(pp, r, hN_r0, H) +
+                                                         o.s * opS(pp, r, hS_r0));
+                    v_s[r * BLOCK3 + tid] = vv;
+                    a[3] += sr[r] * vv;
+                    const int R = R0 + r;
+                    if (R == 0 || R == HH - 1) { pub(R, HV_R, sr[r]); pub(R, HV_V2, vv); }
+                }
+            });
             PMARK(10);
             block_reduce2<4, 1, false>(a, red);
             if (tid == 0) {
@@ -409,49 +427,57 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                         hN[0] = __ldcg(hb_N + HV_S * HALO_ROW); hN[1] = __ldcg(hb_N + HV_T * HALO_ROW);
                         hN[2] = __ldcg(hb_N + HV_P * HALO_ROW); hN[3] = __ldcg(hb_N + HV_V * HALO_ROW);
                     }
-                    #pragma unroll
-                    for (int r = 0; r < RMAX; ++r) {
-                        if (r >= hs) continue;
-                        const int i = r * BLOCK3 + tid;
-                        const double rr = sr[r] - omega * t_s[i];
-                        if (pending) x_s[i] += alpha * pp[r] + omega * sr[r];
-                        const double pn = rr + beta * (pp[r] - omega * v_s[i]);
-                        sr[r] = rr;
-                        pp[r] = pn;
-                        put_op(r, pn);
-                    }
-                    pending = false;
-                    const double haloS = (hS[0] - omega * hS[1]) + beta * (hS[2] - omega * hS[3]);
-                    const double haloN = (hN[0] - omega * hN[1]) + beta * (hN[2] - omega * hN[3]);
-                    __syncthreads();
-                    #pragma unroll
-                    for (int r = 0; r < RMAX; ++r) {
-                        if (r >= hs) continue;
-                        const int si = sidx(r);
-                        const Off o = coef(r);
-                        const double vv = pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] +
-                                                             o.n * opN(pp, r, haloN) + o.s * opS(pp, r, haloS));
-                        v_s[r * BLOCK3 + tid] = vv;
-                        a[0] += BT(r) * vv;
-                        const int R = R0 + r;
-                        if (R == 0 || R == h - 1) { pub(R, HV_R, sr[r]); pub(R, HV_V2, vv); }
-                    }
-                } else if (do_epi) {
-                    #pragma unroll
-                    for (int r = 0; r < RMAX; ++r) {
-                        if (r >= hs) continue;
-                        double dx = X(r);
-                        if (pending) dx += alpha * pp[r] + omega * sr[r];
-                        const long long q = q_of(r);
-                        if (S.mode == 1) S.xptr[me][q] = dx;
-                        else {
-                            pX[q] = dx;
-                            Unew[q] = u_s[uidx(r)] + dx;
+                    with_hs([&](auto tag) {
+                        constexpr int HC = decltype(tag)::value;
+                        const int H = HC ? HC : hs, HH = (HC && Gr == 1) ? HC : h;
+                        #pragma unroll
+                        for (int r = 0; r < RMAX; ++r) {
+                            if (r >= H) continue;
+                            const int i = r * BLOCK3 + tid;
+                            const double rr = sr[r] - omega * t_s[i];
+                            if (pending) x_s[i] += alpha * pp[r] + omega * sr[r];
+                            const double pn = rr + beta * (pp[r] - omega * v_s[i]);
+                            sr[r] = rr;
+                            pp[r] = pn;
+                            put_op(r, pn);
                         }
-                        a[1] += dx * dx;
-                        a[2] = fmax(a[2], fabs(dx));
-                        if (!isfinite(dx)) a[3] = 1.0;
-                    }
+                        const double haloS = (hS[0] - omega * hS[1]) + beta * (hS[2] - omega * hS[3]);
+                        const double haloN = (hN[0] - omega * hN[1]) + beta * (hN[2] - omega * hN[3]);
+                        __syncthreads();
+                        #pragma unroll
+                        for (int r = 0; r < RMAX; ++r) {
+                            if (r >= H) continue;
+                            const int si = sidx(r);
+                            const Off o = coef(r);
+                            const double vv = pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] +
+                                                                 o.n * opNh(pp, r, haloN, H) + o.s * opS(pp, r, haloS));
+                            v_s[r * BLOCK3 + tid] = vv;
+                            a[0] += BT(r) * vv;
+                            const int R = R0 + r;
+                            if (R == 0 || R == HH - 1) { pub(R, HV_R, sr[r]); pub(R, HV_V2, vv); }
+                        }
+                    });
+                    pending = false;
+                } else if (do_epi) {
+                    with_hs([&](auto tag) {
+                        constexpr int HC = decltype(tag)::value;
+                        const int H = HC ? HC : hs;
+                        #pragma unroll
+                        for (int r = 0; r < RMAX; ++r) {
+                            if (r >= H) continue;
+                            double dx = X(r);
+                            if (pending) dx += alpha * pp[r] + omega * sr[r];
+                            const long long q = q_of(r);
+                            if (S.mode == 1) S.xptr[me][q] = dx;
+                            else {
+                                pX[q] = dx;
+                                Unew[q] = u_s[uidx(r)] + dx;
+                            }
+                            a[1] += dx * dx;
+                            a[2] = fmax(a[2], fabs(dx));
+                            if (!isfinite(dx)) a[3] = 1.0;
+                        }
+                    });
                     pending = false;
                 }
                 block_reduce2<2, 2, false>(a, red);
@@ -490,31 +516,35 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     double hS[2] = {0.0, 0.0}, hN[2] = {0.0, 0.0};
                     if (hasS) { hS[0] = __ldcg(hb_S + HV_R * HALO_ROW); hS[1] = __ldcg(hb_S + HV_V2 * HALO_ROW); }
                     if (hasN) { hN[0] = __ldcg(hb_N + HV_R * HALO_ROW); hN[1] = __ldcg(hb_N + HV_V2 * HALO_ROW); }
-                    #pragma unroll
-                    for (int r = 0; r < RMAX; ++r) {
-                        if (r >= hs) continue;
-                        const double sv = sr[r] - alpha * v_s[r * BLOCK3 + tid];
-                        sr[r] = sv;
-                        put_op(r, sv);
-                    }
-                    const double haloS = hS[0] - alpha * hS[1], haloN = hN[0] - alpha * hN[1];
-                    __syncthreads();
-                    #pragma unroll
-                    for (int r = 0; r < RMAX; ++r) {
-                        if (r >= hs) continue;
-                        const int si = sidx(r);
-                        const Off o = coef(r);
-                        const double sv = sr[r];
-                        const double t = sv + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] + o.n * opN(sr, r, haloN) +
-                                                         o.s * opS(sr, r, haloS));
-                        t_s[r * BLOCK3 + tid] = t;
-                        const double b0 = BT(r);
-                        a[0] += t * sv; a[1] += t * t; a[2] += b0 * sv; a[3] += b0 * t; a[4] += sv * sv;
-                        const int R = R0 + r;
-                        if (R == 0 || R == h - 1) {
-                            pub(R, HV_S, sv); pub(R, HV_T, t); pub(R, HV_P, pp[r]); pub(R, HV_V, v_s[r * BLOCK3 + tid]);
+                    with_hs([&](auto tag) {
+                        constexpr int HC = decltype(tag)::value;
+                        const int H = HC ? HC : hs, HH = (HC && Gr == 1) ? HC : h;
+                        #pragma unroll
+                        for (int r = 0; r < RMAX; ++r) {
+                            if (r >= H) continue;
+                            const double sv = sr[r] - alpha * v_s[r * BLOCK3 + tid];
+                            sr[r] = sv;
+                            put_op(r, sv);
                         }
-                    }
+                        const double haloS = hS[0] - alpha * hS[1], haloN = hN[0] - alpha * hN[1];
+                        __syncthreads();
+                        #pragma unroll
+                        for (int r = 0; r < RMAX; ++r) {
+                            if (r >= H) continue;
+                            const int si = sidx(r);
+                            const Off o = coef(r);
+                            const double sv = sr[r];
+                            const double t = sv + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] +
+                                                             o.n * opNh(sr, r, haloN, H) + o.s * opS(sr, r, haloS));
+                            t_s[r * BLOCK3 + tid] = t;
+                            const double b0 = BT(r);
+                            a[0] += t * sv; a[1] += t * t; a[2] += b0 * sv; a[3] += b0 * t; a[4] += sv * sv;
+                            const int R = R0 + r;
+                            if (R == 0 || R == HH - 1) {
+                                pub(R, HV_S, sv); pub(R, HV_T, t); pub(R, HV_P, pp[r]); pub(R, HV_V, v_s[r * BLOCK3 + tid]);
+                            }
+                        }
+                    });
                 }
                 block_reduce2<5, 0, false>(a, red);
                 if (tid == 0 && !conv) {
