@@ -103,13 +103,14 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
 
     for (int step = 1;; ++step) {
         while (klo < newton_max && step > sS[klo] + P.nt - 1) ++klo;
-        int ks[MAXD];
+        // the active iterations are consecutive: k = kbase + a for pair a < A (no local array)
         int A = 0;
-        for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ks[A++] = k;
-        if (S.mode == 1) { A = S.nb; for (int a = 0; a < A; ++a) ks[a] = a; }
+        for (int k = klo; k < newton_max && A < MAXD && sS[k] <= step; ++k) ++A;
+        const int kbase = S.mode == 1 ? 0 : klo;
+        if (S.mode == 1) A = S.nb;
         const int* const asg = s_asg[A];
         const int me = asg[0], g0 = asg[1], g1 = asg[2];
-        const int kme = ks[me];
+        const int kme = kbase + me;
         const int n = S.mode == 1 ? S.blev[me] : step - sS[kme] + 1;
         const int slot = s_kD[kme];
         const int buf = s_kB[kme], nbuf = s_kB[kme + 1];
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         int kc = -1;
         if (S.mode == 0)
             for (int aa = 0; aa < A; ++aa)
-                if (step - sS[ks[aa]] + 1 == P.nt) kc = ks[aa];
+                if (step - sS[kbase + aa] + 1 == P.nt) kc = kbase + aa;
         if (S.mode == 0 && tid == 0) {
             const int so = s_kD[kme];
             lacc[so][0] += pro_s2; lacc[so][1] = fmax(lacc[so][1], pro_mx);
