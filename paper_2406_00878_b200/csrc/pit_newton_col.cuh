@@ -43,10 +43,14 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     __shared__ int sS[MAXK];
     __shared__ double red[NWARP2 * NPART];
     __shared__ double s_hp_big[4 * GMAX2];
-    __shared__ double s_red[5 * GMAX2 + 8];
+    __shared__ double s_red[8];                        // bar_sync_reduce results (N <= 5)
     __shared__ double lacc[MAXD][4];                   // this CTA's norm partials per pipeline slot, summed over levels
     __shared__ double pro_s2, pro_mx, epi_s2, epi_mx;  // thread 0: this CTA's residual / update partials of the step
     __shared__ double prevmax_s;
+    // update norms (sum du^2, max |du|) of the pipeline slot e_slot, per thread: reduced over the CTA only when the
+    // slot's iteration finishes or the CTA changes slot, not in every step's epilogue
+    __shared__ double s_e[2][BLOCK3];
+    s_e[0][tid] = 0.0; s_e[1][tid] = 0.0;
     // this CTA's share of a step with A active pairs (A = 1..MAXD), computed once: pair me, its CTA block [g0, g1),
     // the strip rows [r0, r1) and the CTAs owning the halo rows r0 - 1 / r1 (integer divisions kept off the step path)
     __shared__ int s_asg[MAXD + 1][8];
@@ -78,6 +82,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     __syncthreads();
 
     unsigned ep = 0;
+    int e_slot = -1;
     unsigned hi[2] = {0u, 0u};
     long long prof[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long t_last = clock64();
@@ -142,6 +147,16 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         auto sidx = [&](int r) { return (R0 + r + 1) * W + col + 2; };   // op_s index of own point r
         auto uidx = [&](int r) { return (R0 + r + 1) * W + col + 2; };   // u_s index of own point r
 
+        auto flush_e = [&]() {                         // CTA-uniform: s_e -> lacc[e_slot]
+            double a2[2] = {s_e[0][tid], s_e[1][tid]};
+            s_e[0][tid] = 0.0; s_e[1][tid] = 0.0;
+            block_reduce2<1, 1, false>(a2, red);
+            if (tid == 0) {
+                lacc[e_slot][2] += a2[0];
+                lacc[e_slot][3] = fmax(lacc[e_slot][3], a2[1]);
+                if (!isfinite(a2[0])) atomicOr(&S.bs->err, 1u);   // a non-finite du makes the sum non-finite
+            }
+        };
         double sr[RMAX], pp[RMAX];
         auto X = [&](int r) -> double& { return x_s[r * BLOCK3 + tid]; };
         auto BT = [&](int r) -> double& { return bt_s[r * BLOCK3 + tid]; };
@@ -460,6 +475,10 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     });
                     pending = false;
                 } else if (do_epi) {
+                    if (S.mode == 0 && slot != e_slot) {
+                        if (e_slot >= 0) flush_e();
+                        e_slot = slot;
+                    }
                     with_hs([&](auto tag) {
                         constexpr int HC = decltype(tag)::value;
                         const int H = HC ? HC : hs;
@@ -479,12 +498,22 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                             if (!isfinite(dx)) a[3] = 1.0;
                         }
                     });
+                    if (S.mode == 0) {
+                        s_e[0][tid] += a[1];
+                        s_e[1][tid] = fmax(s_e[1][tid], a[2]);
+                    }
                     pending = false;
                 }
-                block_reduce2<2, 2, false>(a, red);
+                if (do_p1) {
+                    double a1[1] = {a[0]};
+                    block_reduce2<1, 0, false>(a1, red);
+                    a[0] = a1[0];
+                } else if (do_epi && S.mode == 1) {
+                    block_reduce2<2, 2, false>(a, red);
+                }
                 if (tid == 0) {
                     if (do_p1) S.part[((long long)set * G + g) * NPART] = a[0];
-                    if (do_epi) {
+                    if (do_epi && S.mode == 1) {
                         epi_s2 = a[1];
                         epi_mx = a[2];
                         if (a[3] != 0.0) atomicOr(&S.bs->err, 1u);
@@ -597,10 +626,13 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         if (S.mode == 0)
             for (int aa = 0; aa < A; ++aa)
                 if (step - sS[kbase + aa] + 1 == P.nt) kc = kbase + aa;
+        if (kc >= 0 && e_slot == s_kD[kc]) {           // this CTA holds update norms of iteration kc
+            flush_e();
+            e_slot = -1;
+        }
         if (S.mode == 0 && tid == 0) {
             const int so = s_kD[kme];
             lacc[so][0] += pro_s2; lacc[so][1] = fmax(lacc[so][1], pro_mx);
-            lacc[so][2] += epi_s2; lacc[so][3] = fmax(lacc[so][3], epi_mx);
             if (kc >= 0) {
                 const int sa = s_kD[kc];
                 double* hq = S.hpart + ((long long)sa * G + g) * 4;
