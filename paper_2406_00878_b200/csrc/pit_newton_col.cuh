@@ -47,10 +47,10 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     __shared__ double lacc[MAXD][4];                   // this CTA's norm partials per pipeline slot, summed over levels
     __shared__ double pro_s2, pro_mx, epi_s2, epi_mx;  // thread 0: this CTA's residual / update partials of the step
     __shared__ double prevmax_s;
-    // update norms (sum du^2, max |du|) of the pipeline slot e_slot, per thread: reduced over the CTA only when the
-    // slot's iteration finishes or the CTA changes slot, not in every step's epilogue
-    __shared__ double s_e[2][BLOCK3];
-    s_e[0][tid] = 0.0; s_e[1][tid] = 0.0;
+    // Newton norms of the pipeline slot e_slot per thread (sum r^2, max |r|, sum du^2, max |du|): reduced over the
+    // CTA only when the slot's iteration finishes or the CTA changes slot, not in every step
+    __shared__ double s_e[4][BLOCK3];
+    s_e[0][tid] = 0.0; s_e[1][tid] = 0.0; s_e[2][tid] = 0.0; s_e[3][tid] = 0.0;
     // this CTA's share of a step with A active pairs (A = 1..MAXD), computed once: pair me, its CTA block [g0, g1),
     // the strip rows [r0, r1) and the CTAs owning the halo rows r0 - 1 / r1 (integer divisions kept off the step path)
     __shared__ int s_asg[MAXD + 1][8];
@@ -148,15 +148,21 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         auto uidx = [&](int r) { return (R0 + r + 1) * W + col + 2; };   // u_s index of own point r
 
         auto flush_e = [&]() {                         // CTA-uniform: s_e -> lacc[e_slot]
-            double a2[2] = {s_e[0][tid], s_e[1][tid]};
-            s_e[0][tid] = 0.0; s_e[1][tid] = 0.0;
-            block_reduce2<1, 1, false>(a2, red);
+            double a4[4] = {s_e[0][tid], s_e[2][tid], s_e[1][tid], s_e[3][tid]};
+            s_e[0][tid] = 0.0; s_e[1][tid] = 0.0; s_e[2][tid] = 0.0; s_e[3][tid] = 0.0;
+            block_reduce2<2, 2, false>(a4, red);
             if (tid == 0) {
-                lacc[e_slot][2] += a2[0];
-                lacc[e_slot][3] = fmax(lacc[e_slot][3], a2[1]);
-                if (!isfinite(a2[0])) atomicOr(&S.bs->err, 1u);   // a non-finite du makes the sum non-finite
+                lacc[e_slot][0] += a4[0];
+                lacc[e_slot][1] = fmax(lacc[e_slot][1], a4[2]);
+                lacc[e_slot][2] += a4[1];
+                lacc[e_slot][3] = fmax(lacc[e_slot][3], a4[3]);
+                if (!isfinite(a4[1])) atomicOr(&S.bs->err, 1u);   // a non-finite du makes the sum non-finite
             }
         };
+        if (S.mode == 0 && slot != e_slot) {           // CTA-uniform: a new slot for this CTA
+            if (e_slot >= 0) flush_e();
+            e_slot = slot;
+        }
         double sr[RMAX], pp[RMAX];
         auto X = [&](int r) -> double& { return x_s[r * BLOCK3 + tid]; };
         auto BT = [&](int r) -> double& { return bt_s[r * BLOCK3 + tid]; };
@@ -391,14 +397,17 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 }
             });
             PMARK(10);
-            block_reduce2<4, 1, false>(a, red);
+            if (S.mode == 0) {                         // the residual norms go to the slot accumulators
+                s_e[0][tid] += a[1];
+                s_e[1][tid] = fmax(s_e[1][tid], a[4]);
+            }
+            double a3[3] = {a[0], a[2], a[3]};
+            block_reduce2<3, 0, false>(a3, red);
             if (tid == 0) {
                 double* pq = S.part + ((long long)set * G + g) * NPART;
-                pq[0] = a[0];
-                pq[1] = a[2];
-                pq[2] = a[3];
-                pro_s2 = a[1];
-                pro_mx = a[4];
+                pq[0] = a3[0];
+                pq[1] = a3[1];
+                pq[2] = a3[2];
             }
         }
         PMARK(0);
@@ -475,10 +484,6 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     });
                     pending = false;
                 } else if (do_epi) {
-                    if (S.mode == 0 && slot != e_slot) {
-                        if (e_slot >= 0) flush_e();
-                        e_slot = slot;
-                    }
                     with_hs([&](auto tag) {
                         constexpr int HC = decltype(tag)::value;
                         const int H = HC ? HC : hs;
@@ -499,8 +504,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                         }
                     });
                     if (S.mode == 0) {
-                        s_e[0][tid] += a[1];
-                        s_e[1][tid] = fmax(s_e[1][tid], a[2]);
+                        s_e[2][tid] += a[1];
+                        s_e[3][tid] = fmax(s_e[3][tid], a[2]);
                     }
                     pending = false;
                 }
@@ -631,8 +636,6 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             e_slot = -1;
         }
         if (S.mode == 0 && tid == 0) {
-            const int so = s_kD[kme];
-            lacc[so][0] += pro_s2; lacc[so][1] = fmax(lacc[so][1], pro_mx);
             if (kc >= 0) {
                 const int sa = s_kD[kc];
                 double* hq = S.hpart + ((long long)sa * G + g) * 4;

@@ -70,6 +70,36 @@ __device__ __forceinline__ void block_reduce2(double (&a)[NS + NM], double* sm) 
         if (BCAST) __syncthreads();
         return;
     }
+    if constexpr (N >= 3 && N <= 4 && NWARP2 == 16) {
+        // the same for 3..4 values padded to 4: 2 + 1 + 1 + 1 + 1 shuffles; lane l ends with value 2 b4 + b3
+        const int h4 = (l >> 4) & 1, h3 = (l >> 3) & 1;
+        double c[2];
+        #pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const double lo = a[j], hi = j + 2 < N ? a[j + 2] : 0.0;
+            c[j] = op(2 * h4 + j, h4 ? hi : lo, __shfl_xor_sync(0xffffffffu, h4 ? lo : hi, 16));
+        }
+        const int vi = 2 * h4 + h3;
+        double e = op(vi, h3 ? c[1] : c[0], __shfl_xor_sync(0xffffffffu, h3 ? c[0] : c[1], 8));
+        e = op(vi, e, __shfl_xor_sync(0xffffffffu, e, 4));
+        e = op(vi, e, __shfl_xor_sync(0xffffffffu, e, 2));
+        e = op(vi, e, __shfl_xor_sync(0xffffffffu, e, 1));
+        if ((l & 7) == 0 && vi < N) sm[w * N + vi] = e;
+        __syncthreads();
+        if (w == 0) {
+            // lane l: value i = l / 8 over warps l % 8 and + 8, then an 8-lane butterfly; value i ends in lane 8 i
+            const int i = l >> 3, q = l & 7;
+            double v = 0.0;
+            if (i < N) v = op(i, sm[q * N + i], sm[(q + 8) * N + i]);
+            v = op(i, v, __shfl_xor_sync(0xffffffffu, v, 4));
+            v = op(i, v, __shfl_xor_sync(0xffffffffu, v, 2));
+            v = op(i, v, __shfl_xor_sync(0xffffffffu, v, 1));
+            #pragma unroll
+            for (int ii = 0; ii < N; ++ii) a[ii] = __shfl_sync(0xffffffffu, v, 8 * ii);
+        }
+        if (BCAST) __syncthreads();
+        return;
+    }
     #pragma unroll
     for (int i = 0; i < N; ++i)
         #pragma unroll
