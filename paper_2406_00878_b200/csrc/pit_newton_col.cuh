@@ -138,6 +138,24 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         double* const hb_own = S.halo + (long long)g * HALO_CTA + col;
         const double* const hb_S = S.halo + (long long)asg[5] * HALO_CTA + 6 * HALO_ROW + col;
         const double* const hb_N = S.halo + (long long)asg[6] * HALO_CTA + col;
+        // halo values of the next phase, loaded right after the barrier that publishes them (bar_sync_reduce_pre):
+        // phase 2 reads r, v2 -> hv[0], hv[1] (S) and hv[4], hv[5] (N); phase 1 reads s, t, p, v -> hv[0..3], hv[4..7]
+        double hv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const bool hasS_ = hs > 0 && own_top && top_valid, hasN_ = hs > 0 && own_bot && bot_valid;
+        auto pre2 = [&]() {
+            if (hasS_) { hv[0] = __ldcg(hb_S + HV_R * HALO_ROW); hv[1] = __ldcg(hb_S + HV_V2 * HALO_ROW); }
+            if (hasN_) { hv[4] = __ldcg(hb_N + HV_R * HALO_ROW); hv[5] = __ldcg(hb_N + HV_V2 * HALO_ROW); }
+        };
+        auto pre1 = [&]() {
+            if (hasS_) {
+                hv[0] = __ldcg(hb_S + HV_S * HALO_ROW); hv[1] = __ldcg(hb_S + HV_T * HALO_ROW);
+                hv[2] = __ldcg(hb_S + HV_P * HALO_ROW); hv[3] = __ldcg(hb_S + HV_V * HALO_ROW);
+            }
+            if (hasN_) {
+                hv[4] = __ldcg(hb_N + HV_S * HALO_ROW); hv[5] = __ldcg(hb_N + HV_T * HALO_ROW);
+                hv[6] = __ldcg(hb_N + HV_P * HALO_ROW); hv[7] = __ldcg(hb_N + HV_V * HALO_ROW);
+            }
+        };
         auto pub = [&](int R, int v, double val) {     // row R of the strip is a boundary row: publish
             if (R == 0) hb_own[v * HALO_ROW] = val;
             if (R == h - 1) hb_own[(6 + v) * HALO_ROW] = val;
@@ -414,7 +432,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         double bnorm2, rho, r0v0;
         {
             double o[3];
-            bar_sync_reduce<3, 0>(S.bs, G, ep, true, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+            bar_sync_reduce_pre<3, 0>(S.bs, G, ep, true, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red, pre2);
             PMARK(4);
             rho = o[0];                                // (r^0, r0) = ||r0||^2
             bnorm2 = o[1];                             // ||b~||^2: reference of the relative stopping test
@@ -443,15 +461,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 double a[4] = {0.0, 0.0, 0.0, 0.0};        // (b~, v) | sum du^2 | max |du|, nonfinite
                 const bool do_p1 = !conv, do_epi = conv && !epi_done;
                 if (do_p1) {
-                    double hS[4] = {0.0, 0.0, 0.0, 0.0}, hN[4] = {0.0, 0.0, 0.0, 0.0};
-                    if (hasS) {
-                        hS[0] = __ldcg(hb_S + HV_S * HALO_ROW); hS[1] = __ldcg(hb_S + HV_T * HALO_ROW);
-                        hS[2] = __ldcg(hb_S + HV_P * HALO_ROW); hS[3] = __ldcg(hb_S + HV_V * HALO_ROW);
-                    }
-                    if (hasN) {
-                        hN[0] = __ldcg(hb_N + HV_S * HALO_ROW); hN[1] = __ldcg(hb_N + HV_T * HALO_ROW);
-                        hN[2] = __ldcg(hb_N + HV_P * HALO_ROW); hN[3] = __ldcg(hb_N + HV_V * HALO_ROW);
-                    }
+                    const double* const hS = hv;       // pre-loaded after barrier B (pre1)
+                    const double* const hN = hv + 4;
                     with_hs([&](auto tag) {
                         constexpr int HC = decltype(tag)::value;
                         const int H = HC ? HC : hs, HH = (HC && Gr == 1) ? HC : h;
@@ -527,8 +538,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 if (do_epi) epi_done = true;
                 if (do_epi) PMARK(3); else PMARK(1);           // trace: epilogue slot vs phase-1 work
                 double o1[1];
-                const bool any = bar_sync_reduce<1, 0>(S.bs, G, ep, !conv, hi, S.part + (long long)set * G * NPART, NPART,
-                                                       g0, g1, o1, s_red);
+                const bool any = bar_sync_reduce_pre<1, 0>(S.bs, G, ep, !conv, hi, S.part + (long long)set * G * NPART,
+                                                           NPART, g0, g1, o1, s_red, pre2);
                 PMARK(4);
                 if (!any) { set ^= 1; break; }
                 const double r0v = o1[0];
@@ -548,9 +559,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             {
                 double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // (t,s) (t,t) (b~,s) (b~,t) (s,s)
                 if (!conv) {
-                    double hS[2] = {0.0, 0.0}, hN[2] = {0.0, 0.0};
-                    if (hasS) { hS[0] = __ldcg(hb_S + HV_R * HALO_ROW); hS[1] = __ldcg(hb_S + HV_V2 * HALO_ROW); }
-                    if (hasN) { hN[0] = __ldcg(hb_N + HV_R * HALO_ROW); hN[1] = __ldcg(hb_N + HV_V2 * HALO_ROW); }
+                    const double* const hS = hv;       // pre-loaded after barrier A / the phase-1 barrier (pre2)
+                    const double* const hN = hv + 4;
                     with_hs([&](auto tag) {
                         constexpr int HC = decltype(tag)::value;
                         const int H = HC ? HC : hs, HH = (HC && Gr == 1) ? HC : h;
@@ -590,7 +600,8 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             }
             {
                 double o[5];
-                bar_sync_reduce<5, 0>(S.bs, G, ep, false, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red);
+                bar_sync_reduce_pre<5, 0>(S.bs, G, ep, false, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red,
+                                          pre1);
                 PMARK(4);
                 if (!conv) {
                     const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];

@@ -199,10 +199,12 @@ __device__ __forceinline__ bool bar_sync(BarState* b, unsigned G, unsigned& ep, 
 // over the pair's CTAs [g0, g1): lane l loads the partials of CTAs g0 + l, g0 + l + 32, ... (all loads issued
 // together: one L2 round trip) and sums them in that order, then a fixed butterfly — the same order for every
 // value as a single-warp loop, so results are bit-identical run to run.  C = g1 - g0 <= GMAX2 = 160.
-template <int NS, int NM>
-__device__ __forceinline__ bool bar_sync_reduce(BarState* b, unsigned G, unsigned& ep, bool flag, unsigned (&hi)[2],
-                                                const double* part, int stride, int g0, int g1, double (&out)[NS + NM],
-                                                double* sm) {
+// pre() runs in every thread right after the barrier completes, before the partial loads: loads that only need
+// the barrier (the halo rows the next phase reads) then share the partials' L2 round trip.
+template <int NS, int NM, class Pre>
+__device__ __forceinline__ bool bar_sync_reduce_pre(BarState* b, unsigned G, unsigned& ep, bool flag, unsigned (&hi)[2],
+                                                    const double* part, int stride, int g0, int g1,
+                                                    double (&out)[NS + NM], double* sm, Pre&& pre) {
     constexpr int N = NS + NM;
     constexpr int J = GMAX2 / 32;
     __shared__ unsigned s_any2;
@@ -221,6 +223,7 @@ __device__ __forceinline__ bool bar_sync_reduce(BarState* b, unsigned G, unsigne
         hi[ep & 1] = h;
     }
     __syncthreads();
+    pre();
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     if (w < N) {                                        // a warp-uniform condition
         double y[J];
@@ -245,6 +248,13 @@ __device__ __forceinline__ bool bar_sync_reduce(BarState* b, unsigned G, unsigne
     #pragma unroll
     for (int i = 0; i < N; ++i) out[i] = sm[i];
     return any;
+}
+
+template <int NS, int NM>
+__device__ __forceinline__ bool bar_sync_reduce(BarState* b, unsigned G, unsigned& ep, bool flag, unsigned (&hi)[2],
+                                                const double* part, int stride, int g0, int g1, double (&out)[NS + NM],
+                                                double* sm) {
+    return bar_sync_reduce_pre<NS, NM>(b, G, ep, flag, hi, part, stride, g0, g1, out, sm, [] {});
 }
 
 // u at unknown (gc, gr) of level n, extended by the Dirichlet ring (Eq. 2) or the periodic wrap.
