@@ -64,6 +64,8 @@ struct pit_handle {
     double* c_U = nullptr;        // [ntc][nsc] coarse solution
     double* c_fac = nullptr;      // [2][Kmax] spline factors
     int* c_info = nullptr;        // [2]
+    cudaGraphExec_t c_march = nullptr;   // the coarse level march captured once as a CUDA graph (launch overhead)
+    long long c_march_launches = 0;
     char err[512] = {0};
 };
 
@@ -153,6 +155,8 @@ static void free_all(pit_handle* h) {
     cudaFree(h->pf_Y); cudaFree(h->pf_R); cudaFree(h->pf_dU); cudaFree(h->pf_part);
     cudaFree(h->ex_B); cudaFree(h->ex_C5); cudaFree(h->ex_err);
     h->ex_B = h->ex_C5 = nullptr; h->ex_err = nullptr; h->ex_capB = h->ex_capC = 0;
+    if (h->c_march) cudaGraphExecDestroy(h->c_march);
+    h->c_march = nullptr;
     cudaFree(h->c_u0); cudaFree(h->c_ring); cudaFree(h->c_U); cudaFree(h->c_fac); cudaFree(h->c_info);
     h->c_u0 = h->c_ring = h->c_U = h->c_fac = nullptr; h->c_info = nullptr;
     if (h->coarse) { pit_destroy(h->coarse); h->coarse = nullptr; }
@@ -630,13 +634,45 @@ static int build_guess(pit_handle* h, const double* d_u0, const double* d_bc, cu
         CUDA_TRY(h, cudaGetLastError());
         ++nl;
     }
+    // sequential BDF1 on the coarse grid: ntc one-level solves.  Every pointer of the march is
+    // handle-owned, so it is captured once as a CUDA graph and replayed (a level's solve is ~45 us of kernels; the
+    // ~8 API calls that launch it cost about as much again); PIT_GUESS_GRAPH=0 or a failed capture march directly.
+    auto march = [&](cudaStream_t s, long long& cl) -> int {
+        for (int m = 1; m <= g.ntc; ++m) {
+            const double* um1 = m == 1 ? h->c_u0 : h->c_U + (long long)(m - 2) * g.nsc;
+            const double* rg = g.cring ? h->c_ring + (long long)(m - 1) * g.ring_len_c : nullptr;
+            int rc = pit_solve_device(h->coarse, um1, rg, nullptr, h->c_U + (long long)(m - 1) * g.nsc, nullptr, h->c_info, s);
+            if (rc != PIT_OK) return set_err(h, rc, "coarse-grid solve, level %d: %s", m, pit_last_error(h->coarse));
+            cl += h->coarse->launches;
+        }
+        return PIT_OK;
+    };
     long long cl = 0;
-    for (int m = 1; m <= g.ntc; ++m) {                 // sequential BDF1 on the coarse grid
-        const double* um1 = m == 1 ? h->c_u0 : h->c_U + (long long)(m - 2) * g.nsc;
-        const double* rg = g.cring ? h->c_ring + (long long)(m - 1) * g.ring_len_c : nullptr;
-        int rc = pit_solve_device(h->coarse, um1, rg, nullptr, h->c_U + (long long)(m - 1) * g.nsc, nullptr, h->c_info, st);
-        if (rc != PIT_OK) return set_err(h, rc, "coarse-grid solve, level %d: %s", m, pit_last_error(h->coarse));
-        cl += h->coarse->launches;
+    const char* genv = getenv("PIT_GUESS_GRAPH");
+    const bool use_graph = !(genv && atoi(genv) == 0);
+    if (use_graph && !h->c_march) {
+        cudaStream_t cs = nullptr;
+        cudaGraph_t graph = nullptr;
+        long long ccl = 0;
+        bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            const int rc = march(cs, ccl);
+            ok = cudaStreamEndCapture(cs, &graph) == cudaSuccess && rc == PIT_OK && graph &&
+                 cudaGraphInstantiate(&h->c_march, graph, 0) == cudaSuccess;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        if (cs) cudaStreamDestroy(cs);
+        if (!ok) { if (h->c_march) cudaGraphExecDestroy(h->c_march); h->c_march = nullptr; }
+        cudaGetLastError();
+        h->c_march_launches = ccl;
+    }
+    if (use_graph && h->c_march) {
+        CUDA_TRY(h, cudaGraphLaunch(h->c_march, st));
+        cl = h->c_march_launches;
+    } else {
+        int rc = march(st, cl);
+        if (rc != PIT_OK) return rc;
     }
     const int NR = g.bc == 1 ? g.nyc : g.nyc + 1, NC = g.bc == 1 ? g.nxc : g.nxc + 1;
     const long long lines[3] = {(long long)g.ntc * NR, (long long)g.ntc * g.nxu, g.ns};
