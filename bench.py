@@ -158,12 +158,12 @@ BARRIER_US = 1.99
 
 
 def sync_floor(st, nit, t_newton):
-    """The latency floor of the persistent on-chip engines: a wavefront step with i BiCGSTAB iterations costs
-    2 i + 1 grid barriers, plus one norm barrier per Newton iteration; at the isolated barrier
-    cost that many barriers take `ms` of the solve's `t_newton`."""
+    """The latency floor of the persistent on-chip engines: the grid barriers the kernel counted (a wavefront step
+    with i BiCGSTAB iterations costs 2 i + 1, or 2 i with the merged first iteration, plus one norm
+    barrier per Newton iteration); at the isolated barrier cost they take `ms` of the solve's `t_newton`."""
     if st.get("engine", 0) < 2:
         return None
-    n = 2 * st["inner_iterations"] + st["steps"] + nit
+    n = st.get("grid_barriers") or 2 * st["inner_iterations"] + st["steps"] + nit
     ms = n * BARRIER_US * 1e-3
     return {"grid_barriers": n, "us_each_isolated": BARRIER_US, "ms": ms, "frac_of_solve": ms / (t_newton * 1e3),
             "source": "tools/barrier_bench.cu (profiles/r01d/barrier_bench.txt)"}

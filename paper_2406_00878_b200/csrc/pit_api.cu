@@ -484,6 +484,12 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
         S.trace = h->trace;
         S.x0carry = getenv("PIT_X0") ? atoi(getenv("PIT_X0")) : 1;   // default: start from du^{n-1}
         S.halo = h->halo;
+        {   // merged first BiCGSTAB iteration: engine 3 Newton solves on periodic 512-wide grids, strips >= 3 rows
+            const char* me_ = getenv("PIT_MERGE");
+            const int Cmax = (h->G + h->D - 1) / h->D;
+            S.merge = (h->engine == 3 && S.mode == 0 && h->P.bc == PIT_PERIODIC && h->P.nxu == 512 && S.x0carry &&
+                       h->P.nyu / Cmax >= 3 && !(me_ && atoi(me_) == 0)) ? 1 : 0;
+        }
         if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 13 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
         CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
@@ -963,8 +969,9 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
         if (h->guess_timed) CUDA_TRY(h, cudaEventElapsedTime(&t_guess, h->ev[4], h->ev[5]));
         out[17 + MAXK + 6] = (long long)(t_guess * 1e6);
     }
+    if (n > 17 + MAXK + 7) out[17 + MAXK + 7] = s[5];   // grid barriers of the last solve (engine 3; 0 otherwise)
     // trace builds: per-CTA cycle accounts [G][13] after the fixed fields (engine 3 only; tools/skew_run.py)
-    const int base = 17 + MAXK + 7;
+    const int base = 17 + MAXK + 8;
     if (h->trace && h->engine == 3 && n >= base + 13 * h->G) {
         std::vector<unsigned long long> pc((size_t)13 * h->G);
         CUDA_TRY(h, cudaMemcpy(pc.data(), h->trace + 13, pc.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));

@@ -74,6 +74,7 @@ struct SolveParams {
     int x0carry;                 // on-chip engine: start each level solve from du^{n-1} (else 0)
     double* halo;                // column engine: [G][2 sides][6 vectors][512] published boundary rows
     int stop_norm;               // 0: stop on max|dU_k|; 1: on the RMS update norm
+    int merge;                   // column engine, Newton solves: merged first BiCGSTAB iteration (periodic, nx 512)
 };
 
 // Grid barrier state of the on-chip engine (zeroed before every launch).

@@ -265,9 +265,48 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             hN_x = carry_at(r1);
             hN_x2 = x0c ? carry_at(r1 + 1) : 0.0;
         }
+        // merged first iteration (S.merge): r0 two rows deep, i.e. at rows r0 - 2 and r1 + 1 (periodic): their u
+        // E/W, the row beyond, u^{n-1}, and x0 (= the carry) E/W and beyond, loaded while the staging lands
+        const bool mrg = Gr == 1 && S.merge != 0;          // grid-uniform (host: mode 0, periodic, nx 512, h >= 3)
+        double fS[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, fN[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (mrg) {
+            auto at = [&](const double* base, int gr, int gc) -> double {
+                gr = gr < 0 ? gr + nyu : (gr >= nyu ? gr - nyu : gr);
+                gc = gc < 0 ? gc + nxu : (gc >= nxu ? gc - nxu : gc);
+                return __ldcg(base + (long long)gr * nxu + gc);
+            };
+            const bool cx = n > 1;
+            if (hasS) {
+                fS[0] = at(Ulev, r0 - 2, col + 1); fS[1] = at(Ulev, r0 - 2, col - 1); fS[2] = at(Ulev, r0 - 3, col);
+                fS[3] = at(uprev, r0 - 2, col);
+                if (cx) { fS[4] = at(pX, r0 - 2, col + 1); fS[5] = at(pX, r0 - 2, col - 1); fS[6] = at(pX, r0 - 3, col); }
+            }
+            if (hasN) {
+                fN[0] = at(Ulev, r1 + 1, col + 1); fN[1] = at(Ulev, r1 + 1, col - 1); fN[2] = at(Ulev, r1 + 2, col);
+                fN[3] = at(uprev, r1 + 1, col);
+                if (cx) { fN[4] = at(pX, r1 + 1, col + 1); fN[5] = at(pX, r1 + 1, col - 1); fN[6] = at(pX, r1 + 2, col); }
+            }
+        }
         PMARK(7);
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
+        // r0 = b~ - A~ x0 at a far halo row from its stencil values (u, u^{n-1}, carry; x0 = carry)
+        auto r0_far = [&](double uc, double ue, double uw, double un, double us, double up, double xc, double xe,
+                          double xw, double xn, double xs) -> double {
+            const Vals v = {uc, ue, uw, un, us};
+            double G, aC;
+            res_diag<LAW>(P, v, up, G, aC);
+            const double ci = LAW == 1 ? ci_const : 1.0 / aC;
+            const double bt = (-G + (n == 1 ? 0.0 : xc)) * ci;
+            if (!x0c) return bt;
+            const Off o = offdiag_law<LAW>(P, v);
+            return bt - (xc + ci * (o.e * xe + o.w * xw + o.n * xn + o.s * xs));
+        };
+        double rfS = 0.0, rfN = 0.0;                       // r0 at rows r0 - 2 and r1 + 1
+        if (mrg && hasS)
+            rfS = r0_far(hS_u2, fS[0], fS[1], u_s[uidx(-1)], fS[2], fS[3], hS_x2, fS[4], fS[5], hS_x, fS[6]);
+        if (mrg && hasN)
+            rfN = r0_far(hN_u2, fN[0], fN[1], fN[2], u_s[uidx(hs)], fN[3], hN_x2, fN[4], fN[5], fN[6], hN_x);
         if (S.mode == 0) {
             #pragma unroll
             for (int r = 0; r < RMAX; ++r) {
@@ -310,6 +349,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         double hS_r0 = 0.0, hN_r0 = 0.0;       // r0 = p0 on the halo rows
         {
             double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // sum r0^2, sum r^2, sum b~^2, sum r0 v0 | max |r|
+            double am[4] = {0.0, 0.0, 0.0, 0.0};      // merged: (v0,v0), (r0,w0), (v0,w0), (w0,w0)
             with_hs([&](auto tag) {
                 constexpr int HC = decltype(tag)::value;
                 const int H = HC ? HC : hs, HH = (HC && Gr == 1) ? HC : h;
@@ -399,6 +439,10 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     a[0] += sr[r] * sr[r];
                     put_op(r, sr[r]);
                 }
+                if (mrg) {                                 // r0 on the halo rows: E/W operands of v0 there
+                    if (hasS) put_op_at(sidx(-1), hS_r0);
+                    if (hasN) put_op_at(sidx(H), hN_r0);
+                }
                 __syncthreads();
                 // v0 = A~ p0; publish r0, v0 of the boundary rows (the halo of phase 2)
                 #pragma unroll
@@ -410,8 +454,49 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                                                          o.s * opS(pp, r, hS_r0));
                     v_s[r * BLOCK3 + tid] = vv;
                     a[3] += sr[r] * vv;
+                    am[0] += vv * vv;
                     const int R = R0 + r;
                     if (R == 0 || R == HH - 1) { pub(R, HV_R, sr[r]); pub(R, HV_V2, vv); }
+                }
+                if (mrg) {
+                    // merged first iteration: v0 on the halo rows (r0 two rows deep), then w0 = A~ v0 on own rows, so
+                    // that every dot product of the first iteration is a polynomial in alpha of one reduction
+                    double v0S = 0.0, v0N = 0.0;
+                    if (hasS) {
+                        const int si = sidx(-1);
+                        v0S = hS_r0 + hS_ci * (hS_o.e * op_s[si + dE] + hS_o.w * op_s[si + dW] + hS_o.n * sr[0] +
+                                               hS_o.s * rfS);
+                    }
+                    if (hasN) {
+                        const int si = sidx(H);
+                        double rl = 0.0;                   // r0 at the last own row (select chain, no dynamic index)
+                        #pragma unroll
+                        for (int r = 0; r < RMAX; ++r) rl = fma(r == H - 1 ? 1.0 : 0.0, sr[r], rl);
+                        v0N = hN_r0 + hN_ci * (hN_o.e * op_s[si + dE] + hN_o.w * op_s[si + dW] + hN_o.n * rfN +
+                                               hN_o.s * rl);
+                    }
+                    __syncthreads();                       // all reads of r0 in op_s done
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) {
+                        if (r >= H) continue;
+                        pp[r] = v_s[r * BLOCK3 + tid];
+                        put_op(r, pp[r]);
+                    }
+                    if (hasS) put_op_at(sidx(-1), v0S);
+                    if (hasN) put_op_at(sidx(H), v0N);
+                    __syncthreads();
+                    #pragma unroll
+                    for (int r = 0; r < RMAX; ++r) {
+                        if (r >= H) continue;
+                        const int si = sidx(r);
+                        const Off o = coef(r);
+                        const double w0 = pp[r] + cinv(r) * (o.e * op_s[si + dE] + o.w * op_s[si + dW] +
+                                                             o.n * opNh(pp, r, v0N, H) + o.s * opS(pp, r, v0S));
+                        t_s[r * BLOCK3 + tid] = w0;
+                        am[1] += sr[r] * w0; am[2] += pp[r] * w0; am[3] += w0 * w0;
+                        const int R = R0 + r;
+                        if (R == 0 || R == HH - 1) pub(R, HV_T, w0);
+                    }
                 }
             });
             PMARK(10);
@@ -419,24 +504,51 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 s_e[0][tid] += a[1];
                 s_e[1][tid] = fmax(s_e[1][tid], a[4]);
             }
-            double a3[3] = {a[0], a[2], a[3]};
-            block_reduce2<3, 0, false>(a3, red);
-            if (tid == 0) {
-                double* pq = S.part + ((long long)set * G + g) * NPART;
-                pq[0] = a3[0];
-                pq[1] = a3[1];
-                pq[2] = a3[2];
+            if (mrg) {
+                double a7[7] = {a[0], a[2], a[3], am[0], am[1], am[2], am[3]};
+                block_reduce2<7, 0, false>(a7, red);
+                if (tid == 0) {
+                    double* pq = S.part + ((long long)set * G + g) * NPART;
+                    for (int j = 0; j < 7; ++j) pq[j] = a7[j];
+                }
+            } else {
+                double a3[3] = {a[0], a[2], a[3]};
+                block_reduce2<3, 0, false>(a3, red);
+                if (tid == 0) {
+                    double* pq = S.part + ((long long)set * G + g) * NPART;
+                    pq[0] = a3[0];
+                    pq[1] = a3[1];
+                    pq[2] = a3[2];
+                }
             }
         }
         PMARK(0);
         double bnorm2, rho, r0v0;
+        double o7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         {
-            double o[3];
-            bar_sync_reduce_pre<3, 0>(S.bs, G, ep, true, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red, pre2);
+            if (mrg) {
+                auto prem = [&]() {                    // the neighbours' r0, v0, w0 boundary rows
+                    if (hasS_) {
+                        hv[0] = __ldcg(hb_S + HV_R * HALO_ROW); hv[1] = __ldcg(hb_S + HV_V2 * HALO_ROW);
+                        hv[2] = __ldcg(hb_S + HV_T * HALO_ROW);
+                    }
+                    if (hasN_) {
+                        hv[4] = __ldcg(hb_N + HV_R * HALO_ROW); hv[5] = __ldcg(hb_N + HV_V2 * HALO_ROW);
+                        hv[6] = __ldcg(hb_N + HV_T * HALO_ROW);
+                    }
+                };
+                bar_sync_reduce_pre<7, 0>(S.bs, G, ep, true, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o7, s_red,
+                                          prem);
+            } else {
+                double o[3];
+                bar_sync_reduce_pre<3, 0>(S.bs, G, ep, true, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red,
+                                          pre2);
+                o7[0] = o[0]; o7[1] = o[1]; o7[2] = o[2];
+            }
             PMARK(4);
-            rho = o[0];                                // (r^0, r0) = ||r0||^2
-            bnorm2 = o[1];                             // ||b~||^2: reference of the relative stopping test
-            r0v0 = o[2];                               // (r^0, v0)
+            rho = o7[0];                               // (r^0, r0) = ||r0||^2
+            bnorm2 = o7[1];                            // ||b~||^2: reference of the relative stopping test
+            r0v0 = o7[2];                              // (r^0, v0)
         }
         PMARK(5);
         set ^= 1;
@@ -452,6 +564,61 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         }
         int it = 0, maxit_step = 0;
         bool fused_first = true;                       // iteration 0's phase 1 happened in the prologue
+        // the scalar update that follows a phase-2 reduction (t = A s): omega, the residual estimate, the stop test,
+        // beta and the new rho (Jacobi-scaled BiCGSTAB)
+        auto after_phase2 = [&](double ts, double tt2, double r0s, double r0t, double ss) {
+            ++it;
+            pending = true;
+            if (tt2 == 0.0) {
+                omega = 0.0;
+                conv = true;
+            } else {
+                omega = ts / tt2;
+                const double rhon = r0s - omega * r0t;
+                const double rn2 = fmax(ss - 2.0 * omega * ts + omega * omega * tt2, 0.0);
+                if (!isfinite(omega) || !isfinite(rn2)) {
+                    if (tid == 0 && c == 0) atomicOr(&S.bs->err, 1u);
+                    conv = true;
+                } else if (rn2 <= rtol2 * bnorm2 || rn2 <= atol2 || it >= S.lin_max) {
+                    conv = true;
+                } else if (omega == 0.0 || rhon == 0.0) {
+                    if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
+                    conv = true;
+                } else {
+                    beta = (rhon / rho) * (alpha / omega);
+                    rho = rhon;
+                }
+            }
+        };
+        if (mrg) {
+            // merged first iteration: with s = r0 - alpha v0 and t = A~ s = v0 - alpha w0, every dot product of the
+            // first phase 2 is a polynomial in alpha of the reduced (r0, v0, w0) products: no second barrier
+            if (!conv) {
+                const double vv = o7[3], rw = o7[4], vw = o7[5], ww = o7[6];
+                after_phase2(r0v0 - alpha * vv - alpha * rw + alpha * alpha * vw,     // (t, s)
+                             vv - 2.0 * alpha * vw + alpha * alpha * ww,                 // (t, t)
+                             rho - alpha * r0v0,                                         // (r^0, s)
+                             r0v0 - alpha * rw,                                          // (r^0, t)
+                             rho - 2.0 * alpha * r0v0 + alpha * alpha * vv);             // (s, s)
+                #pragma unroll
+                for (int r = 0; r < RMAX; ++r) {
+                    if (r >= hs) continue;
+                    const int i = r * BLOCK3 + tid;
+                    const double v0 = v_s[i];
+                    sr[r] = sr[r] - alpha * v0;        // s
+                    t_s[i] = v0 - alpha * t_s[i];      // t (t_s held w0)
+                    pp[r] = BT(r);                     // p = r0
+                }
+                // the neighbours' boundary rows as the (s, t, p, v) the phase-1 slot expects
+                for (int side = 0; side < 2; ++side) {
+                    double* q = hv + 4 * side;
+                    const double r0h = q[0], v0h = q[1], w0h = q[2];
+                    q[0] = r0h - alpha * v0h; q[1] = v0h - alpha * w0h; q[2] = r0h; q[3] = v0h;
+                }
+                maxit_step = it;
+            }
+            fused_first = false;
+        }
 
         // Control flow around every block / pair reduction is uniform across the CTA (converged pairs reduce
         // zeros).
@@ -603,31 +770,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 bar_sync_reduce_pre<5, 0>(S.bs, G, ep, false, hi, S.part + (long long)set * G * NPART, NPART, g0, g1, o, s_red,
                                           pre1);
                 PMARK(4);
-                if (!conv) {
-                    const double ts = o[0], tt2 = o[1], r0s = o[2], r0t = o[3], ss = o[4];
-                    ++it;
-                    pending = true;
-                    if (tt2 == 0.0) {
-                        omega = 0.0;
-                        conv = true;
-                    } else {
-                        omega = ts / tt2;
-                        const double rhon = r0s - omega * r0t;
-                        const double rn2 = fmax(ss - 2.0 * omega * ts + omega * omega * tt2, 0.0);
-                        if (!isfinite(omega) || !isfinite(rn2)) {
-                            if (tid == 0 && c == 0) atomicOr(&S.bs->err, 1u);
-                            conv = true;
-                        } else if (rn2 <= rtol2 * bnorm2 || rn2 <= atol2 || it >= S.lin_max) {
-                            conv = true;
-                        } else if (omega == 0.0 || rhon == 0.0) {
-                            if (tid == 0 && c == 0) atomicOr(&S.bs->err, 2u);
-                            conv = true;
-                        } else {
-                            beta = (rhon / rho) * (alpha / omega);
-                            rho = rhon;
-                        }
-                    }
-                }
+                if (!conv) after_phase2(o[0], o[1], o[2], o[3], o[4]);
             }
             set ^= 1;
             maxit_step = it > maxit_step ? it : maxit_step;
@@ -720,7 +863,10 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
             if (g == 0 && tid == 0) {
                 S.info[0] = kf;
                 S.info[1] = stop_status;
-                if (S.stats) { S.stats[0] = step; S.stats[1] = total_inner; S.stats[2] = S.D; S.stats[3] = G; }
+                if (S.stats) {
+                    S.stats[0] = step; S.stats[1] = total_inner; S.stats[2] = S.D; S.stats[3] = G;
+                    S.stats[5] = ep;                   // grid barriers every CTA passed
+                }
             }
             flush_prof();
             return;

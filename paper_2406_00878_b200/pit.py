@@ -172,13 +172,13 @@ class Solver:
                                                             _stream(stream)))
 
     def stats(self):
-        out = (C.c_int64 * (17 + 256 + 7))()
-        self._check(lib().pit_stats(self.h, out, 17 + 256 + 7))
+        out = (C.c_int64 * (17 + 256 + 8))()
+        self._check(lib().pit_stats(self.h, out, 17 + 256 + 8))
         d = {"steps": out[0], "inner_iterations": out[1], "depth": out[2], "grid": out[3], "launches": out[4],
              "newton_kernel_ms": out[5] * 1e-6, "init_kernel_ms": out[6] * 1e-6, "engine": out[7],
              "product_form": bool(out[15]), "explicit_form": out[15] == 2, "pair_iterations": out[16],
              "iterations_per_newton_k": [out[17 + k] for k in range(256) if out[17 + k]],
-             "guess_ms": out[279] * 1e-6}
+             "guess_ms": out[279] * 1e-6, "grid_barriers": out[280]}
         if any(out[8:15]):
             names = ["prologue", "phase1", "phase2", "epilogue", "barrier", "reduce", "step_tail"]
             d["trace_cycles_per_cta"] = {k: out[8 + i] / max(1, out[3]) for i, k in enumerate(names)}

@@ -22,7 +22,7 @@ for _ in range(2):
     s.solve_device(d_u0, None, None, d_out, d_hist, d_info)
 st = s.stats()
 G, D = st["grid"], st["depth"]
-base = 17 + 256 + 7
+base = 17 + 256 + 8
 n = base + 13 * G
 out = (C.c_int64 * n)()
 pit.lib().pit_stats(s.h, out, n)
