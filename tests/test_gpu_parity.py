@@ -255,3 +255,25 @@ def test_column_engine_strip_shapes(nx, ny, nt, depth):
     assert normwise_rel(U3, U1) <= 1e-13
     for k in range(n3):
         assert abs(h3[k, 3] - h1[k, 3]) <= 1e-8 * h1[k, 3] + 1e-2 * p.newton_tol   # + the update rounding floor
+
+
+@pytest.mark.parametrize("nt", [1, 2, 9])
+def test_merged_first_iteration(nt, monkeypatch):
+    """The merged first BiCGSTAB iteration (periodic 512-wide grids: w0 = A~ v0 formed in the prologue, the first
+    phase 2 from polynomials in alpha) against the two-barrier path and the oracle's sequential
+    solve: same converged solution (1e-10), one grid barrier per wavefront step fewer."""
+    p = W.config(5, nt=nt)
+    res = {}
+    for m in ("1", "0"):
+        monkeypatch.setenv("PIT_MERGE", m)
+        U, hist, nit, st, stats = gpu_solve(p)
+        assert st in (pit.PIT_OK, pit.PIT_OK_FLOOR), (m, st, hist)
+        res[m] = (U, nit, stats)
+    (U1, n1, s1), (U0, n0, s0) = res["1"], res["0"]
+    assert s1["engine"] == 3 and s0["engine"] == 3
+    assert normwise_rel(U1, U0) <= 1e-10
+    # one barrier per wavefront step fewer (plus identical norm barriers when the iteration counts agree)
+    if n1 == n0 and s1["steps"] == s0["steps"] and s1["inner_iterations"] == s0["inner_iterations"]:
+        assert s0["grid_barriers"] - s1["grid_barriers"] == s1["steps"]
+    seq = O.solve_sequential(p, levels=min(nt, 2))
+    assert normwise_rel(U1[:seq.U.shape[0]], seq.U) <= 1e-10
