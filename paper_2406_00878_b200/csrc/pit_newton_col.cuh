@@ -45,7 +45,6 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
     __shared__ double s_hp_big[4 * GMAX2];
     __shared__ double s_red[8];                        // bar_sync_reduce results (N <= 5)
     __shared__ double lacc[MAXD][4];                   // this CTA's norm partials per pipeline slot, summed over levels
-    __shared__ double pro_s2, pro_mx, epi_s2, epi_mx;  // thread 0: this CTA's residual / update partials of the step
     __shared__ double prevmax_s;
     // Newton norms of the pipeline slot e_slot per thread (sum r^2, max |r|, sum du^2, max |du|): reduced over the
     // CTA only when the slot's iteration finishes or the CTA changes slot, not in every step
@@ -141,17 +140,17 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         // halo values of the next phase, loaded right after the barrier that publishes them (bar_sync_reduce_pre):
         // phase 2 reads r, v2 -> hv[0], hv[1] (S) and hv[4], hv[5] (N); phase 1 reads s, t, p, v -> hv[0..3], hv[4..7]
         double hv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        const bool hasS_ = hs > 0 && own_top && top_valid, hasN_ = hs > 0 && own_bot && bot_valid;
+        const bool hasS = hs > 0 && own_top && top_valid, hasN = hs > 0 && own_bot && bot_valid;
         auto pre2 = [&]() {
-            if (hasS_) { hv[0] = __ldcg(hb_S + HV_R * HALO_ROW); hv[1] = __ldcg(hb_S + HV_V2 * HALO_ROW); }
-            if (hasN_) { hv[4] = __ldcg(hb_N + HV_R * HALO_ROW); hv[5] = __ldcg(hb_N + HV_V2 * HALO_ROW); }
+            if (hasS) { hv[0] = __ldcg(hb_S + HV_R * HALO_ROW); hv[1] = __ldcg(hb_S + HV_V2 * HALO_ROW); }
+            if (hasN) { hv[4] = __ldcg(hb_N + HV_R * HALO_ROW); hv[5] = __ldcg(hb_N + HV_V2 * HALO_ROW); }
         };
         auto pre1 = [&]() {
-            if (hasS_) {
+            if (hasS) {
                 hv[0] = __ldcg(hb_S + HV_S * HALO_ROW); hv[1] = __ldcg(hb_S + HV_T * HALO_ROW);
                 hv[2] = __ldcg(hb_S + HV_P * HALO_ROW); hv[3] = __ldcg(hb_S + HV_V * HALO_ROW);
             }
-            if (hasN_) {
+            if (hasN) {
                 hv[4] = __ldcg(hb_N + HV_S * HALO_ROW); hv[5] = __ldcg(hb_N + HV_T * HALO_ROW);
                 hv[6] = __ldcg(hb_N + HV_P * HALO_ROW); hv[7] = __ldcg(hb_N + HV_V * HALO_ROW);
             }
@@ -192,7 +191,6 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         // barrier.  r0 on the two halo rows (needed by v0) is recomputed redundantly by the edge threads from
         // u (two rows deep), u^{n-1} and the carry, all of which are inputs of this step.
         const bool x0c = S.x0carry && S.mode == 0 && n > 1;
-        const bool hasS = hs > 0 && own_top && top_valid, hasN = hs > 0 && own_bot && bot_valid;
         // stage u of the strip, rows -1 .. h, in 16-byte pieces (cp.async.cg: every thread copies column pairs of
         // whole rows, independent of the column it owns; periodic rows wrap).  Dirichlet ring rows and the E/W halo
         // columns (the ring) are written with ordinary stores.
@@ -316,15 +314,11 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         PMARK(8);
         // operand accessors: N/S from registers inside the sub-strip, shared memory across the column-group
         // boundary, the halo register across the CTA boundary; E/W from shared memory
-        auto opN = [&](const double (&o)[RMAX], int r, double haloN) -> double {
-            if (r + 1 < hs) return o[r + 1];
-            return own_bot ? haloN : op_s[sidx(r) + W];
-        };
         auto opS = [&](const double (&o)[RMAX], int r, double haloS) -> double {
             if (r > 0) return o[r - 1];
             return own_top ? haloS : op_s[sidx(r) - W];
         };
-        auto opNh = [&](const double (&o)[RMAX], int r, double haloN, int H) -> double {   // opN for H = hs
+        auto opNh = [&](const double (&o)[RMAX], int r, double haloN, int H) -> double {   // H = hs
             if (r + 1 < H) return o[r + 1];
             return own_bot ? haloN : op_s[sidx(r) + W];
         };
@@ -528,11 +522,11 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         {
             if (mrg) {
                 auto prem = [&]() {                    // the neighbours' r0, v0, w0 boundary rows
-                    if (hasS_) {
+                    if (hasS) {
                         hv[0] = __ldcg(hb_S + HV_R * HALO_ROW); hv[1] = __ldcg(hb_S + HV_V2 * HALO_ROW);
                         hv[2] = __ldcg(hb_S + HV_T * HALO_ROW);
                     }
-                    if (hasN_) {
+                    if (hasN) {
                         hv[4] = __ldcg(hb_N + HV_R * HALO_ROW); hv[5] = __ldcg(hb_N + HV_V2 * HALO_ROW);
                         hv[6] = __ldcg(hb_N + HV_T * HALO_ROW);
                     }
@@ -696,11 +690,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                 }
                 if (tid == 0) {
                     if (do_p1) S.part[((long long)set * G + g) * NPART] = a[0];
-                    if (do_epi && S.mode == 1) {
-                        epi_s2 = a[1];
-                        epi_mx = a[2];
-                        if (a[3] != 0.0) atomicOr(&S.bs->err, 1u);
-                    }
+                    if (do_epi && S.mode == 1 && a[3] != 0.0) atomicOr(&S.bs->err, 1u);
                 }
                 if (do_epi) epi_done = true;
                 if (do_epi) PMARK(3); else PMARK(1);           // trace: epilogue slot vs phase-1 work
