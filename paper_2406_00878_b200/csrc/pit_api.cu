@@ -484,10 +484,10 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
         S.trace = h->trace;
         S.x0carry = getenv("PIT_X0") ? atoi(getenv("PIT_X0")) : 1;   // default: start from du^{n-1}
         S.halo = h->halo;
-        {   // merged first BiCGSTAB iteration: engine 3 Newton solves on periodic 512-wide grids, strips >= 3 rows
+        {   // merged first BiCGSTAB iteration: engine 3 Newton solves on periodic grids, strips >= 3 rows
             const char* me_ = getenv("PIT_MERGE");
             const int Cmax = (h->G + h->D - 1) / h->D;
-            S.merge = (h->engine == 3 && S.mode == 0 && h->P.bc == PIT_PERIODIC && h->P.nxu == 512 && S.x0carry &&
+            S.merge = (h->engine == 3 && S.mode == 0 && h->P.bc == PIT_PERIODIC && S.x0carry &&
                        h->P.nyu / Cmax >= 3 && !(me_ && atoi(me_) == 0)) ? 1 : 0;
         }
         if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 13 * sizeof(unsigned long long), st));

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
         }
         // merged first iteration (S.merge): r0 two rows deep, i.e. at rows r0 - 2 and r1 + 1 (periodic): their u
         // E/W, the row beyond, u^{n-1}, and x0 (= the carry) E/W and beyond, loaded while the staging lands
-        const bool mrg = Gr == 1 && S.merge != 0;          // grid-uniform (host: mode 0, periodic, nx 512, h >= 3)
+        const bool mrg = S.merge != 0;                     // grid-uniform (host: mode 0, periodic, strips >= 3 rows)
         double fS[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, fN[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         if (mrg) {
             auto at = [&](const double* base, int gr, int gc) -> double {

@@ -257,12 +257,13 @@ def test_column_engine_strip_shapes(nx, ny, nt, depth):
         assert abs(h3[k, 3] - h1[k, 3]) <= 1e-8 * h1[k, 3] + 1e-2 * p.newton_tol   # + the update rounding floor
 
 
-@pytest.mark.parametrize("nt", [1, 2, 9])
-def test_merged_first_iteration(nt, monkeypatch):
-    """The merged first BiCGSTAB iteration (periodic 512-wide grids: w0 = A~ v0 formed in the prologue, the first
-    phase 2 from polynomials in alpha) against the two-barrier path and the oracle's sequential
-    solve: same converged solution (1e-10), one grid barrier per wavefront step fewer."""
-    p = W.config(5, nt=nt)
+@pytest.mark.parametrize("c,nt", [(5, 1), (5, 2), (5, 9), (4, 2), (4, 17)])
+def test_merged_first_iteration(c, nt, monkeypatch):
+    """The merged first BiCGSTAB iteration (periodic grids of the column engine, one column group at 512 wide, two
+    at 256: w0 = A~ v0 formed in the prologue, the first phase 2 from polynomials in alpha) against
+    the two-barrier path and the oracle's sequential solve: same converged solution (1e-10), one grid barrier per
+    wavefront step fewer."""
+    p = W.config(c, nt=nt)
     res = {}
     for m in ("1", "0"):
         monkeypatch.setenv("PIT_MERGE", m)
