@@ -187,8 +187,10 @@ __device__ __forceinline__ bool bar_sync(BarState* b, unsigned G, unsigned& ep, 
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
         } while ((unsigned)v < target);
         const unsigned h = (unsigned)(v >> 32);
-        s_any = h != hi[ep & 1];
-        hi[ep & 1] = h;
+        // static indices (a dynamic hi[ep & 1] would put the pair in local memory, on every barrier's path)
+        const bool odd = (ep & 1) != 0;
+        s_any = h != (odd ? hi[1] : hi[0]);
+        if (odd) hi[1] = h; else hi[0] = h;
     }
     ++ep;
     __syncthreads();
@@ -219,8 +221,10 @@ __device__ __forceinline__ bool bar_sync_reduce_pre(BarState* b, unsigned G, uns
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
         } while ((unsigned)v < target);
         const unsigned h = (unsigned)(v >> 32);
-        s_any2 = h != hi[ep & 1];
-        hi[ep & 1] = h;
+        // static indices (a dynamic hi[ep & 1] would put the pair in local memory, on every barrier's path)
+        const bool odd = (ep & 1) != 0;
+        s_any2 = h != (odd ? hi[1] : hi[0]);
+        if (odd) hi[1] = h; else hi[0] = h;
     }
     __syncthreads();
     pre();
