@@ -604,10 +604,11 @@ __global__ void __launch_bounds__(BLOCK3, 1) k_newton_col(SolveParams S) {
                     pp[r] = BT(r);                     // p = r0
                 }
                 // the neighbours' boundary rows as the (s, t, p, v) the phase-1 slot expects
-                for (int side = 0; side < 2; ++side) {
-                    double* q = hv + 4 * side;
-                    const double r0h = q[0], v0h = q[1], w0h = q[2];
-                    q[0] = r0h - alpha * v0h; q[1] = v0h - alpha * w0h; q[2] = r0h; q[3] = v0h;
+                #pragma unroll
+                for (int side = 0; side < 2; ++side) {     // unrolled: hv stays in registers
+                    const int b = 4 * side;
+                    const double r0h = hv[b], v0h = hv[b + 1], w0h = hv[b + 2];
+                    hv[b] = r0h - alpha * v0h; hv[b + 1] = v0h - alpha * w0h; hv[b + 2] = r0h; hv[b + 3] = v0h;
                 }
                 maxit_step = it;
             }
