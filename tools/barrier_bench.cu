@@ -4,6 +4,7 @@
 //   1: red.release arrival, ld.relaxed spin + fence.acq_rel.gpu after it
 //   2: variant 0 with __nanosleep(32) between polls
 //   3: variant 0 without the partial loads (barrier only)
+//   4: variant 0 with 4 staggered pollers (lane 0 of warps 0..3)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o barrier_bench barrier_bench.cu
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -18,7 +19,25 @@ __global__ void __launch_bounds__(512, 1) bench(unsigned long long* ctr, double*
         double* pset = part + (size_t)(it & 1) * G * 8;
         if (threadIdx.x < 5) pset[g * 8 + threadIdx.x] = acc + threadIdx.x + it;
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (V == 4) {
+            // 4 pollers (lane 0 of warps 0..3) staggered by ~1/4 of an L2 round trip; the first to see the
+            // barrier complete raises a shared flag the others watch
+            __shared__ volatile int done;
+            if (threadIdx.x == 0) done = 0;
+            __syncthreads();
+            unsigned long long* c = ctr + 16 * (it & 1);
+            const unsigned long long target = (unsigned long long)(it / 2 + 1) * G;
+            if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(c) : "memory");
+            if ((threadIdx.x & 31) == 0 && w < 4) {
+                if (w) __nanosleep(80 * w);
+                unsigned long long v;
+                for (;;) {
+                    if (done) break;
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+                    if (v >= target) { done = 1; break; }
+                }
+            }
+        } else if (threadIdx.x == 0) {
             unsigned long long* c = ctr + 16 * (it & 1);
             asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(c) : "memory");
             const unsigned long long target = (unsigned long long)(it / 2 + 1) * G;
@@ -71,9 +90,10 @@ int main() {
     unsigned long long* ctr; double *part, *out;
     cudaMalloc(&ctr, 256); cudaMalloc(&part, 2 * G * 8 * sizeof(double)); cudaMalloc(&out, 8);
     for (int rep = 0; rep < 2; ++rep) {
-        printf("G=%d: v0 acquire spin + partials %.3f us | v1 relaxed spin + fence %.3f us | v2 nanosleep %.3f us | v3 barrier only %.3f us\n", G,
+        printf("G=%d: v0 acquire spin + partials %.3f us | v1 relaxed spin + fence %.3f us | v2 nanosleep %.3f us | v3 barrier only %.3f us | v4 4 staggered pollers %.3f us\n", G,
                1e3 * run<0>(G, ctr, part, out, iters) / iters, 1e3 * run<1>(G, ctr, part, out, iters) / iters,
-               1e3 * run<2>(G, ctr, part, out, iters) / iters, 1e3 * run<3>(G, ctr, part, out, iters) / iters);
+               1e3 * run<2>(G, ctr, part, out, iters) / iters, 1e3 * run<3>(G, ctr, part, out, iters) / iters,
+               1e3 * run<4>(G, ctr, part, out, iters) / iters);
     }
     return 0;
 }
