@@ -267,11 +267,13 @@ def test_merged_first_iteration(c, nt, monkeypatch):
     res = {}
     for m in ("1", "0"):
         monkeypatch.setenv("PIT_MERGE", m)
-        U, hist, nit, st, stats = gpu_solve(p)
+        # the recurrence path (AUTO would take the product form for these short horizons)
+        U, hist, nit, st, stats = gpu_solve(p, inverse_mode=pit.PIT_INV_RECURRENCE)
         assert st in (pit.PIT_OK, pit.PIT_OK_FLOOR), (m, st, hist)
         res[m] = (U, nit, stats)
     (U1, n1, s1), (U0, n0, s0) = res["1"], res["0"]
     assert s1["engine"] == 3 and s0["engine"] == 3
+    assert s1["steps"] > 0 and s1["grid_barriers"] > 0          # the persistent kernel ran
     assert normwise_rel(U1, U0) <= 1e-10
     # one barrier per wavefront step fewer (plus identical norm barriers when the iteration counts agree)
     if n1 == n0 and s1["steps"] == s0["steps"] and s1["inner_iterations"] == s0["inner_iterations"]:
