@@ -183,9 +183,11 @@ __device__ __forceinline__ bool bar_sync(BarState* b, unsigned G, unsigned& ep, 
         asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(add) : "memory");
         const unsigned target = (ep / 2 + 1) * G;
         unsigned long long v;
-        do {
+        for (;;) {                                     // 32 ns back-off between polls (tools/barrier_bench.cu)
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-        } while ((unsigned)v < target);
+            if ((unsigned)v >= target) break;
+            __nanosleep(32);
+        }
         const unsigned h = (unsigned)(v >> 32);
         // static indices (a dynamic hi[ep & 1] would put the pair in local memory, on every barrier's path)
         const bool odd = (ep & 1) != 0;
@@ -217,9 +219,11 @@ __device__ __forceinline__ bool bar_sync_reduce_pre(BarState* b, unsigned G, uns
         asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(add) : "memory");
         const unsigned target = (ep / 2 + 1) * G;
         unsigned long long v;
-        do {
+        for (;;) {                                     // 32 ns back-off between polls (tools/barrier_bench.cu)
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-        } while ((unsigned)v < target);
+            if ((unsigned)v >= target) break;
+            __nanosleep(32);
+        }
         const unsigned h = (unsigned)(v >> 32);
         // static indices (a dynamic hi[ep & 1] would put the pair in local memory, on every barrier's path)
         const bool odd = (ep & 1) != 0;
