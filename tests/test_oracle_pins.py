@@ -147,3 +147,28 @@ def test_eq15_and_remark4():
         assert PF.count_nonzero_diagonals(P[n - 1]) == 2 * n * n + 2 * n + 1
     # beyond 2n >= N_x the offsets alias and the count falls short of the formula
     assert PF.count_nonzero_diagonals(P[7]) < 2 * 8 * 8 + 2 * 8 + 1
+
+
+def test_fullsize_golden_manifest_integrity():
+    """tests/golden/fullsize/ (written by tools/make_fullsize_golden.py from oracle/ only): files match their sha256,
+    shapes match the configs, and the stored levels agree with the per-level fingerprints."""
+    import hashlib
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fullsize")
+    man = json.load(open(os.path.join(gold, "MANIFEST.json")))
+    assert sorted(man) == ["c2", "c3", "c4", "c5"]
+    for key, rec in man.items():
+        c = int(key[1:])
+        p = W.config(c)
+        for f, h in ((f"{key}_levels.npy", rec["levels_sha256"]), (f"{key}_stats.npy", rec["stats_sha256"])):
+            assert hashlib.sha256(open(os.path.join(gold, f), "rb").read()).hexdigest() == h, f
+        lv = np.load(os.path.join(gold, f"{key}_levels.npy"))
+        fp = np.load(os.path.join(gold, f"{key}_stats.npy"))
+        assert lv.shape == (4, p.ns) and fp.shape == (p.nt, 3)
+        assert rec["levels"] == [p.nt // 4, p.nt // 2, 3 * p.nt // 4, p.nt]
+        for i, n in enumerate(rec["levels"]):
+            assert abs(lv[i].sum() - fp[n - 1, 0]) <= 1e-9 * p.ns
+            assert abs(np.abs(lv[i]).max() - fp[n - 1, 2]) == 0.0
+        if p.bc == W.PERIODIC:   # exact mass conservation of periodic Burgers at every stored level
+            assert np.abs(fp[:, 0] - p.u0.sum()).max() <= 1e-12 * p.ns
