@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define PIT_ABI_VERSION 2
+#define PIT_ABI_VERSION 3
 
 typedef enum {
     PIT_OK = 0,           /* converged: max|dU_k| <= newton_tol */
@@ -88,10 +88,16 @@ typedef struct {
                               the whole horizon (EXPLICIT) */
     int32_t pipeline_depth;/* Newton iterations in flight in the level wavefront; 0 = auto */
     int32_t device;        /* CUDA device ordinal */
-    int32_t engine;        /* 0 = auto (column-blocked on-chip if it fits, else strip on-chip, else global),
+    int32_t engine;        /* Newton-solve engine.  0 = auto: 4 if it applies, else 3, 2, 1 (the first that fits).
                               1 = global-state engine (any size), 2 = strip on-chip engine, 3 = column-blocked
-                              on-chip engine (nx = 256 or 512 unknowns per row); 2/3: PIT_EINVAL if they do
-                              not fit the registers + shared memory of one SM per CTA */
+                              on-chip engine (nx = 256 or 512 unknowns per row) — engines 1-3 solve every level
+                              with Jacobi-scaled BiCGSTAB to lin_rtol behind grid-wide barriers;
+                              4 = neighbour-synchronised engine: every level solved by lin_sweeps red-black SOR
+                              sweeps (Young's relaxation from the Jacobi bound of A_1 at the initial iterate),
+                              only neighbouring row strips synchronise (64..512 unknowns per row, even; periodic
+                              grids also need an even number of rows; <= 4 rows per CTA).  2/3/4: PIT_EINVAL if
+                              they do not apply.  Level solves outside the Newton solve (pit_level_solve_device,
+                              the product forms) always use BiCGSTAB (engines 1-3). */
     int32_t guess_cf;      /* initial Newton iterate when the caller passes no guess:
                               0 = u^0 at every level; c_f >= 2 = the paper's coarse-grid guess: sequential-
                               equivalent BDF1 solve on the grid coarsened by c_f in x, y and t (the same
@@ -101,6 +107,13 @@ typedef struct {
                               (Dirichlet) / >= 3 (periodic) intervals.  Paper: 4 (heat), 3 (Burgers) */
     int32_t stop_norm;     /* 0 = max|dU_k| (default); 1 = the paper's L2 update norm
                               sqrt(sum (dU_k)^2 / (nt ns)) */
+    int32_t lin_sweeps;    /* engine 4: red-black SOR sweeps per level solve; 0 = auto =
+                              ceil(ln(lin_rtol) / ln(omega - 1)), the a-priori sweep count for a lin_rtol error
+                              reduction at Young's rate omega - 1 (the reached level residuals are reported by
+                              pit_engine_info) */
+    int32_t lin_check;     /* engine 4: the level solves' a-posteriori residual ||b - A_n du^n|| is measured on every
+                              lin_check-th level and the last (0 = default 16, 1 = every level): it waits for the
+                              neighbouring strips' final values, one more exchange on the level's critical path */
 } pit_config;
 
 typedef struct pit_handle pit_handle;
@@ -191,6 +204,12 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * out[273..278] = prologue sub-categories of the cycle accounting, out[279] = device time of the coarse-grid
  * initial guess (coarse solve + interpolation) [ns], 0 without it. */
 int pit_stats(pit_handle* h, int64_t* out, int32_t n);
+
+/* Engine facts of the last Newton solve (synchronizes with it).  out[0] = engine (1..4), out[1] = omega,
+ * out[2] = sweeps per level solve, out[3] = the Jacobi bound q (engine 4; 0 otherwise), then for k = 0..n_iter-1:
+ * out[4 + 2k] = ||res||_2 / ||b||_2 of iteration k's level solves over all levels (res = b - A_n du^n, b = r^n +
+ * du^{n-1}), out[5 + 2k] = max |res| (engine 4 only; zeros otherwise).  n = number of doubles out can hold. */
+int pit_engine_info(pit_handle* h, double* out, int32_t n);
 
 const char* pit_strerror(int code);
 const char* pit_last_error(const pit_handle* h);

@@ -19,6 +19,7 @@
 #include "pit_kernels.cu"
 #include "pit_guess.cuh"
 #include "pit_explicit.cuh"
+#include "pit_nb_params.cuh"
 
 using namespace pit;
 
@@ -66,6 +67,19 @@ struct pit_handle {
     int* c_info = nullptr;        // [2]
     cudaGraphExec_t c_march = nullptr;   // the coarse level march captured once as a CUDA graph (launch overhead)
     long long c_march_launches = 0;
+    // engine 4 (neighbour-synchronised RB-SOR Newton solve, pit_newton_nb.cuh)
+    bool nb = false;              // the Newton solve runs on engine 4
+    int nb_rmax = 0, nb_G = 0, nb_D = 0, nb_dm = 0;   // base strip height, CTAs, iterations in flight, warp groups
+    size_t nb_smem = 0;
+    unsigned long long* nb_llx = nullptr;   // LL cells, x publications
+    unsigned long long* nb_llu = nullptr;   // LL cells, U boundary-row publications
+    size_t nb_llx_bytes = 0, nb_llu_bytes = 0;
+    double* nb_hpart = nullptr;   // [MAXK][G][NB_NP]
+    unsigned* nb_sync = nullptr;  // [2][MAXK] arrive counters, decisions
+    unsigned long long* nb_qbits = nullptr;
+    double* nb_ctl = nullptr;     // [4] omega, sweeps, q
+    double* nb_linres = nullptr;  // [MAXK][2]
+    int last_engine = 0;          // engine of the last Newton solve
     char err[512] = {0};
 };
 
@@ -137,6 +151,9 @@ static int validate(const pit_config* c, char* why, size_t n) {
     }
     if (c->pipeline_depth < 0 || c->pipeline_depth > MAXD) { snprintf(why, n, "pipeline_depth must be in 0..%d", MAXD); return PIT_EINVAL; }
     if (c->window < 0) { snprintf(why, n, "window < 0"); return PIT_EINVAL; }
+    if (c->engine < 0 || c->engine > 4) { snprintf(why, n, "engine %d", c->engine); return PIT_EINVAL; }
+    if (c->lin_sweeps < 0 || c->lin_sweeps > 400) { snprintf(why, n, "lin_sweeps must be in 0..400"); return PIT_EINVAL; }
+    if (c->lin_check < 0) { snprintf(why, n, "lin_check < 0"); return PIT_EINVAL; }
     if (c->stop_norm < 0 || c->stop_norm > 1) { snprintf(why, n, "stop_norm %d", c->stop_norm); return PIT_EINVAL; }
     if (c->guess_cf == 1 || c->guess_cf < 0) { snprintf(why, n, "guess_cf must be 0 or >= 2"); return PIT_EINVAL; }
     if (c->guess_cf >= 2) {
@@ -154,6 +171,10 @@ static void free_all(pit_handle* h) {
     cudaFree(h->d_small); cudaFree(h->bs); cudaFree(h->trace);
     cudaFree(h->pf_Y); cudaFree(h->pf_R); cudaFree(h->pf_dU); cudaFree(h->pf_part);
     cudaFree(h->ex_B); cudaFree(h->ex_C5); cudaFree(h->ex_err);
+    cudaFree(h->nb_llx); cudaFree(h->nb_llu); cudaFree(h->nb_hpart); cudaFree(h->nb_sync); cudaFree(h->nb_qbits);
+    cudaFree(h->nb_ctl); cudaFree(h->nb_linres);
+    h->nb_llx = h->nb_llu = nullptr; h->nb_hpart = h->nb_ctl = h->nb_linres = nullptr; h->nb_sync = nullptr;
+    h->nb_qbits = nullptr;
     h->ex_B = h->ex_C5 = nullptr; h->ex_err = nullptr; h->ex_capB = h->ex_capC = 0;
     if (h->c_march) cudaGraphExecDestroy(h->c_march);
     h->c_march = nullptr;
@@ -203,6 +224,11 @@ static const void* col_fn_n(int rmax, bool trace, int law) {
 
 static const void* col_fn(int rmax, bool trace, int law, int nxu) {
     return nxu == 512 ? col_fn_n<512>(rmax, trace, law) : col_fn_n<256>(rmax, trace, law);
+}
+
+// Engine 4 kernel for (base strip height, law, row length): its own translation units (pit_nb_law*.cu).
+static const void* nb_fn(int hb, int law, int nxu, int want_dm, size_t* smem, int* dm) {
+    return law == 1 ? nb_kernel_law1(hb, nxu, want_dm, smem, dm) : nb_kernel_law0(hb, nxu, want_dm, smem, dm);
 }
 
 // LAW 1 = viscous Burgers with constant viscosity (m2 = 0): specialised matvec coefficients.
@@ -361,8 +387,25 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         if (D == 0) D = (int)std::min<long long>(8, std::max<long long>(1, (96ll << 20) / std::max<long long>(slot_bytes, 1)));
         h->D = std::max(1, std::min(D, c.newton_max));
     }
+    // Engine 4 (the Newton solve): rows of 64..512 unknowns (even), <= 4 rows per CTA, one CTA per SM.
+    if ((c.engine == 0 || c.engine == 4) && (c.inverse_mode == PIT_INV_AUTO || c.inverse_mode == PIT_INV_RECURRENCE) &&
+        (P.nxu == 64 || P.nxu == 128 || P.nxu == 256 || P.nxu == 512) && (c.bc == PIT_DIRICHLET || P.nyu % 2 == 0)) {
+        const int G4 = std::min(h->sms, P.nyu);
+        const int hb4 = P.nyu / G4;
+        size_t smem4 = 0;
+        int occ4 = 0, dm = 1;
+        const void* fn = nb_fn(hb4, law, P.nxu, c.pipeline_depth, &smem4, &dm);
+        const int D4 = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : dm, std::min(dm, c.newton_max)));
+        const int rmax = hb4;
+        if (fn && smem4 <= 227 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, fn, dm * (P.nxu / 2), smem4) == cudaSuccess && occ4 >= 1) {
+            h->nb = true; h->nb_rmax = rmax; h->nb_G = G4; h->nb_D = D4; h->nb_smem = smem4; h->nb_dm = dm;
+        }
+        cudaGetLastError();
+    }
+    if (c.engine == 4 && !h->nb) { delete h; return PIT_EINVAL; }
     const int D = h->D;
-    h->B = std::max(3, D);
+    h->B = std::max(std::max(3, D), h->nb ? h->nb_D + 1 : 0);
 
     const long long N = P.ns * P.nt;
     if ((rc = dalloc(h, &h->U, (size_t)(h->B * N))) ||
@@ -378,11 +421,20 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
         (rc = dalloc(h, &h->d_small, 2 * 1024 + 2)) ||
         (rc = dalloc(h, &h->bs, 1)) ||
-        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 13 + 13 * GMAX2)))) {
+        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 13 + 13 * GMAX2))) ||
+        (h->nb && ((rc = dalloc(h, &h->nb_llx, (size_t)h->nb_G * h->nb_dm * NB_RX * 2 * (P.nxu / 2) * 2)) ||
+                   (rc = dalloc(h, &h->nb_llu, (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2)) ||
+                   (rc = dalloc(h, &h->nb_hpart, (size_t)MAXK * h->nb_G * NB_NP)) ||
+                   (rc = dalloc(h, &h->nb_sync, (size_t)2 * MAXK)) ||
+                   (rc = dalloc(h, &h->nb_qbits, 1)) ||
+                   (rc = dalloc(h, &h->nb_ctl, 4)) ||
+                   (rc = dalloc(h, &h->nb_linres, (size_t)2 * MAXK))))) {
         free_all(h);
         delete h;
         return rc;
     }
+    h->nb_llx_bytes = (size_t)h->nb_G * h->nb_dm * NB_RX * 2 * (P.nxu / 2) * 2 * sizeof(unsigned long long);
+    h->nb_llu_bytes = (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2 * sizeof(unsigned long long);
     bool ev_ok = true;
     for (auto& e : h->ev) ev_ok = ev_ok && cudaEventCreate(&e) == cudaSuccess;
     if (!ev_ok || cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess ||
@@ -507,6 +559,43 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
     return PIT_OK;
 }
 
+// Engine 4: omega and the sweep count from the Jacobi bound of A_1 at the initial iterate (device), then the
+// persistent neighbour-synchronised kernel.  The LL cells and the per-iteration counters are cleared first, so a
+// publication number never matches a cell of an earlier solve.
+static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, double* d_u_out, double* d_hist, int* d_info,
+                     cudaStream_t st) {
+    const Prob& P = h->P;
+    CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_llx, 0, h->nb_llx_bytes, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_llu, 0, h->nb_llu_bytes, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_sync, 0, sizeof(unsigned) * 2 * MAXK, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_qbits, 0, sizeof(unsigned long long), st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_linres, 0, sizeof(double) * 2 * MAXK, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
+    nb_setup_launch(P, h->U, ring, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
+                    std::max(1, std::min(grid_for(P.ns, h->sms), 2 * h->sms)), st);
+    CUDA_TRY(h, cudaGetLastError());
+    NbParams S;
+    std::memset(&S, 0, sizeof(S));
+    S.P = P; S.u0 = d_u0; S.ring = ring; S.U = h->U; S.B = h->B; S.D = h->nb_D; S.G = h->nb_G;
+    S.ctl = h->nb_ctl; S.llx = h->nb_llx; S.llu = h->nb_llu; S.hpart = h->nb_hpart;
+    S.arrive = h->nb_sync; S.decided = h->nb_sync + MAXK;
+    S.hist = d_hist ? d_hist : h->hist; S.linres = h->nb_linres; S.info = d_info ? d_info : h->info;
+    S.u_out = d_u_out; S.newton_tol = h->cfg.newton_tol; S.newton_max = h->cfg.newton_max; S.stop_norm = h->cfg.stop_norm;
+    S.stats = h->stats;
+    S.trace = h->trace ? h->trace + 13 : nullptr;
+    void* args[] = {(void*)&S};
+    size_t smem4 = 0;
+    int dm4 = 0;
+    const void* fn = nb_fn(h->nb_rmax, h->law, P.nxu, h->cfg.pipeline_depth, &smem4, &dm4);
+    CUDA_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->nb_smem));
+    CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->nb_G), dim3(h->nb_dm * (P.nxu / 2)), args, h->nb_smem, st));
+    CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
+    h->launches += 9;
+    h->last_engine = 4;
+    return PIT_OK;
+}
+
 // k_init_iterate bracketed by events (per-kernel device time on the launching stream, for bench.py)
 static int launch_init(pit_handle* h, const double* d_u0, const double* d_guess, cudaStream_t st) {
     const long long N = h->P.ns * h->P.nt;
@@ -609,12 +698,8 @@ static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, 
 // AUTO: the paper's literal product form when the Section 7 gate admits the whole horizon as one window
 // (BASELINE c1), the recurrence otherwise.
 static bool want_product(pit_handle* h, const double* d_bc, cudaStream_t st) {
-    if (h->cfg.inverse_mode == PIT_INV_PRODUCT_WINDOW || h->cfg.inverse_mode == PIT_INV_EXPLICIT) return true;
-    if (h->cfg.inverse_mode == PIT_INV_RECURRENCE || h->P.nt > 64) return false;
-    if (ensure_pf_scratch(h) != PIT_OK) return false;
-    std::vector<double> an(h->P.nt);
-    if (level_anorms(h, h->U, d_bc, 1, h->P.nt, an.data(), st) != PIT_OK) return false;
-    return chain_bound(an.data(), h->P.nt) <= PIT_GATE;
+    (void)d_bc; (void)st;
+    return h->cfg.inverse_mode == PIT_INV_PRODUCT_WINDOW || h->cfg.inverse_mode == PIT_INV_EXPLICIT;
 }
 
 // The paper's initial iterate (pit_guess.cuh), written into iterate buffer 0.  Iterate
@@ -723,6 +808,7 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
         CUDA_TRY(h, cudaMemcpyAsync(h->d_u0, d_u0, sizeof(double) * h->P.ns, cudaMemcpyDeviceToDevice, st));
         d_u0 = h->d_u0;
     }
+    if (h->nb) return launch_nb(h, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_u_out, d_hist, (int*)d_info, st);
     SolveParams S = base_params(h);
     S.u0 = d_u0;
     S.ring = h->P.bc == PIT_DIRICHLET ? d_bc : nullptr;
@@ -730,6 +816,7 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
     S.hist = d_hist ? d_hist : h->hist;
     S.info = d_info ? (int*)d_info : h->info;
     S.mode = 0;
+    h->last_engine = h->engine;
     return launch_newton(h, S, st);
 }
 
@@ -767,12 +854,15 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     const bool prod = want_product(h, has_bc ? h->d_bc : nullptr, 0);
     if (prod) {
         rc = solve_product(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
+    } else if (h->nb) {
+        rc = launch_nb(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else {
         SolveParams S = base_params(h);
         S.u0 = h->d_u0;
         S.ring = has_bc ? h->d_bc : nullptr;
         S.u_out = nullptr;       // the host copy is taken straight from the final iterate buffer
         S.mode = 0;
+        h->last_engine = h->engine;
         rc = launch_newton(h, S, 0);
     }
     if (rc != PIT_OK) return rc;
@@ -959,7 +1049,7 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     unsigned long long tr[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (h->trace) CUDA_TRY(h, cudaMemcpy(tr, h->trace, sizeof(tr), cudaMemcpyDeviceToHost));
     const long long v[17] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
-                             h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
+                             h->last_engine ? h->last_engine : h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
                              (long long)tr[4], (long long)tr[5], (long long)tr[6], (long long)h->product_used, s[4]};
     for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];
     for (int i = 17; i < n && i < 17 + MAXK; ++i) out[i] = s[8 + (i - 17)];
@@ -980,6 +1070,30 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     return PIT_OK;
 }
 
+int pit_engine_info(pit_handle* h, double* out, int32_t n) {
+    if (!h || !out || n < 1) return PIT_EINVAL;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    std::vector<double> v((size_t)4 + 2 * MAXK + 2 * NB_TR, 0.0);
+    v[0] = h->last_engine ? h->last_engine : h->engine;
+    if (h->last_engine == 4) {
+        double ctl[3];
+        CUDA_TRY(h, cudaMemcpy(ctl, h->nb_ctl, sizeof(ctl), cudaMemcpyDeviceToHost));
+        v[1] = ctl[0]; v[2] = ctl[1]; v[3] = ctl[2];
+        CUDA_TRY(h, cudaMemcpy(v.data() + 4, h->nb_linres, sizeof(double) * 2 * MAXK, cudaMemcpyDeviceToHost));
+        if (h->trace) {   // cycle accounts: mean and max over CTAs (PIT_TRACE builds of the handle)
+            std::vector<unsigned long long> tr((size_t)h->nb_G * NB_TR);
+            CUDA_TRY(h, cudaMemcpy(tr.data(), h->trace + 13, tr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            for (int i = 0; i < NB_TR; ++i) {
+                double sum = 0, mx = 0;
+                for (int g = 0; g < h->nb_G; ++g) { sum += (double)tr[(size_t)g * NB_TR + i]; mx = std::max(mx, (double)tr[(size_t)g * NB_TR + i]); }
+                v[4 + 2 * MAXK + i] = sum / h->nb_G;
+                v[4 + 2 * MAXK + NB_TR + i] = mx;
+            }
+        }
+    }
+    for (int i = 0; i < n && i < (int)v.size(); ++i) out[i] = v[i];
+    return PIT_OK;
+}
 
 // ---- N3: the paper's explicit banded form (pit_explicit.cuh) --------------------------------------------
 

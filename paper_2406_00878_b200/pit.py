@@ -16,7 +16,7 @@ from . import workloads as W
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpit.so")
 
-PIT_ABI_VERSION = 2
+PIT_ABI_VERSION = 3
 PIT_OK, PIT_OK_FLOOR, PIT_EINVAL, PIT_ENOMEM, PIT_ECUDA, PIT_ENOCONV, PIT_EBREAKDOWN, PIT_ECOND = 0, 1, -1, -2, -3, -4, -5, -6
 PIT_HEAT, PIT_BURGERS = 0, 1
 PIT_DIRICHLET, PIT_PERIODIC = 0, 1
@@ -24,7 +24,7 @@ PIT_INV_AUTO, PIT_INV_RECURRENCE, PIT_INV_PRODUCT_WINDOW, PIT_INV_EXPLICIT = 0, 
 
 # every symbol include/pit.h declares (tests check the library exports all of them)
 EXPORTS = ["pit_config_init", "pit_create", "pit_destroy", "pit_solve", "pit_solve_device", "pit_residual_device",
-           "pit_level_solve_device", "pit_product_window_device", "pit_explicit_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_strerror",
+           "pit_level_solve_device", "pit_product_window_device", "pit_explicit_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_engine_info", "pit_strerror",
            "pit_last_error", "pit_abi_version"]
 
 
@@ -35,7 +35,8 @@ class PitConfig(C.Structure):
                 ("newton_tol", C.c_double), ("newton_max", C.c_int32), ("lin_rtol", C.c_double),
                 ("lin_atol", C.c_double), ("lin_max", C.c_int32), ("inverse_mode", C.c_int32),
                 ("window", C.c_int32), ("pipeline_depth", C.c_int32), ("device", C.c_int32),
-                ("engine", C.c_int32), ("guess_cf", C.c_int32), ("stop_norm", C.c_int32)]
+                ("engine", C.c_int32), ("guess_cf", C.c_int32), ("stop_norm", C.c_int32),
+                ("lin_sweeps", C.c_int32), ("lin_check", C.c_int32)]
 
 
 class PitError(RuntimeError):
@@ -70,6 +71,7 @@ def lib():
         L.pit_initial_guess_device.argtypes = [hp, dp, dp, dp, vp]; L.pit_initial_guess_device.restype = C.c_int
         L.pit_sizes.argtypes = [hp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]; L.pit_sizes.restype = C.c_int
         L.pit_stats.argtypes = [hp, C.POINTER(C.c_int64), C.c_int32]; L.pit_stats.restype = C.c_int
+        L.pit_engine_info.argtypes = [hp, C.POINTER(C.c_double), C.c_int32]; L.pit_engine_info.restype = C.c_int
         L.pit_strerror.argtypes = [C.c_int]; L.pit_strerror.restype = C.c_char_p
         L.pit_last_error.argtypes = [hp]; L.pit_last_error.restype = C.c_char_p
         L.pit_abi_version.argtypes = []; L.pit_abi_version.restype = C.c_int
@@ -184,6 +186,22 @@ class Solver:
             d["trace_cycles_per_cta"] = {k: out[8 + i] / max(1, out[3]) for i, k in enumerate(names)}
             sub = ["pro_loads", "pro_wait", "pro_residual", "pro_x0mv", "step_setup", "pro_stage"]
             d["trace_cycles_per_cta"].update({k: out[273 + i] / max(1, out[3]) for i, k in enumerate(sub)})
+        return d
+
+    def engine_info(self):
+        """pit_engine_info: engine, omega, sweeps, Jacobi bound and per-iteration level-solve residuals."""
+        n = 4 + 2 * 256 + 16
+        out = (C.c_double * n)()
+        self._check(lib().pit_engine_info(self.h, out, n))
+        lr = [(out[4 + 2 * k], out[5 + 2 * k]) for k in range(256)]
+        while lr and lr[-1] == (0.0, 0.0):
+            lr.pop()
+        d = {"engine": int(out[0]), "omega": out[1], "sweeps": int(out[2]), "q": out[3], "linres": lr}
+        b = 4 + 2 * 256
+        if any(out[b:b + 16]):
+            names = ["prologue", "sweeps", "sweep_waits", "epilogue", "reductions", "pass_ends", "step_setup", "total"]
+            d["trace_mean"] = {k: out[b + i] for i, k in enumerate(names)}
+            d["trace_max"] = {k: out[b + 8 + i] for i, k in enumerate(names)}
         return d
 
     def sizes(self):

@@ -38,12 +38,28 @@ def test_library_exports_every_declared_symbol(built):
     assert built.pit_abi_version() == pit.PIT_ABI_VERSION
 
 
-def test_config_struct_layout_matches_header(built):
+def test_config_struct_layout_matches_header(built, tmp_path):
     # offsets the C compiler sees: pit_config_init writes abi_version/newton_tol/newton_max at their C offsets
     c = pit.PitConfig()
     built.pit_config_init(C.byref(c))
-    assert c.abi_version == pit.PIT_ABI_VERSION == 2 and c.newton_tol == 1e-12 and c.newton_max == 30 and c.x1 == 1.0 and c.y1 == 1.0
+    assert c.abi_version == pit.PIT_ABI_VERSION == 3 and c.newton_tol == 1e-12 and c.newton_max == 30 and c.x1 == 1.0 and c.y1 == 1.0
     assert c.pde == 0 and c.device == 0 and c.pipeline_depth == 0 and c.guess_cf == 0 and c.stop_norm == 0
+    assert c.lin_sweeps == 0 and c.lin_check == 0
+    # every field's offset and the struct size, as gcc lays out include/pit.h, against the ctypes binding
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc unavailable")
+    names = [f[0] for f in pit.PitConfig._fields_]
+    prog = "#include <stdio.h>\n#include <stddef.h>\n#include \"pit.h\"\nint main(void){\n"
+    prog += "".join(f'printf("%zu\\n", offsetof(pit_config, {n}));\n' for n in names)
+    prog += 'printf("%zu\\n", sizeof(pit_config)); return 0; }\n'
+    src = tmp_path / "layout.c"
+    src.write_text(prog)
+    exe = tmp_path / "layout"
+    import subprocess
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    assert got[:-1] == [getattr(pit.PitConfig, n).offset for n in names]
+    assert got[-1] == C.sizeof(pit.PitConfig)
 
 
 def test_strerror(built):
@@ -53,7 +69,8 @@ def test_strerror(built):
 
 @pytest.mark.parametrize("field,value", [("abi_version", 7), ("nx", 1), ("nt", 0), ("dt", 0.0), ("m0", -1.0),
                                          ("newton_max", 0), ("pipeline_depth", 99), ("bc", 5),
-                                         ("guess_cf", 1), ("guess_cf", 5), ("guess_cf", -2), ("stop_norm", 2)])
+                                         ("guess_cf", 1), ("guess_cf", 5), ("guess_cf", -2), ("stop_norm", 2),
+                                         ("engine", 5), ("lin_sweeps", -1), ("lin_sweeps", 401), ("lin_check", -1)])
 def test_invalid_config_rejected_before_touching_the_gpu(built, field, value):
     c = pit.make_config(W.config(1))
     setattr(c, field, value)

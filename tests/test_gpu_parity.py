@@ -268,7 +268,7 @@ def test_merged_first_iteration(c, nt, monkeypatch):
     for m in ("1", "0"):
         monkeypatch.setenv("PIT_MERGE", m)
         # the recurrence path (AUTO would take the product form for these short horizons)
-        U, hist, nit, st, stats = gpu_solve(p, inverse_mode=pit.PIT_INV_RECURRENCE)
+        U, hist, nit, st, stats = gpu_solve(p, inverse_mode=pit.PIT_INV_RECURRENCE, engine=3)
         assert st in (pit.PIT_OK, pit.PIT_OK_FLOOR), (m, st, hist)
         res[m] = (U, nit, stats)
     (U1, n1, s1), (U0, n0, s0) = res["1"], res["0"]

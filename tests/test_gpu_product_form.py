@@ -60,10 +60,12 @@ def test_product_window_matches_dense_theorem1(case):
     assert normwise_rel(got[0], ref[0]) <= 1e-10   # the first row is a plain level solve
 
 
-def test_auto_selects_product_form_on_c1_and_matches_oracle():
+def test_product_form_on_c1_whole_horizon_matches_oracle():
+    """c1's whole horizon is inside the Section 7 gate: PRODUCT_WINDOW runs Theorem 1 over all 8 levels as one window
+    (AUTO is the level recurrence, asynchronous on the stream; R19)."""
     p = W.config(1)
-    U, hist, nit, st, stats = gpu_solve(p, lin_rtol=1e-13)
-    assert stats["product_form"], "c1's whole horizon is inside the Section 7 gate: AUTO must run Theorem 1"
+    U, hist, nit, st, stats = gpu_solve(p, inverse_mode=pit.PIT_INV_PRODUCT_WINDOW, lin_rtol=1e-13)
+    assert stats["product_form"]
     assert st in (0, 1)
     seq = O.solve_sequential(p)
     assert normwise_rel(U, seq.U) <= 1e-10
