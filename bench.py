@@ -8,8 +8,9 @@ iterations / s, plus achieved HBM GB/s of the dominant kernel against MEASURED_P
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl mine|reference]
 
-N > 1 (torchrun, one process per GPU): the path does not shard (replicas only),
-so every rank solves its own replica; value = all ranks' DOF x iterations / max-over-ranks time.
+N > 1 (torchrun, one process per GPU; without WORLD_SIZE in the environment bench.py relaunches itself under
+torchrun with N processes): the headline config does not shard (replicas), so every rank solves its
+own replica; value = all ranks' DOF x iterations / max-over-ranks time.
 --impl reference: the CPU oracle (sequential BDF1 + Newton, 1 core) on a bounded prefix of the same
 workload; rank 0 only.
 """
@@ -85,6 +86,29 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def relaunch_under_torchrun(n):
+    """--gpus N > 1 without a launcher: run N ranks with torchrun on this node (127.0.0.1) and pass the exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -147,7 +171,7 @@ def run_reference(args):
             "config": {"workload": p.name, "nt": p.nt, "grid": [p.nxu, p.nyu], "newton_tol": p.newton_tol},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"sequential BDF1+Newton, levels 1..{L} of {p.nt} at full {p.nxu}x{p.nyu} "
-                                       f"(causal prefix), single thread"},
+                                       f"(causal prefix), single thread", **cpu_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -155,13 +179,29 @@ def run_reference(args):
 
 # Grid barrier + pair reduction on B200, measured in isolation (tools/barrier_bench.cu, profiles/r01d/barrier_bench.txt)
 BARRIER_US = 1.99
+# One neighbour-exchange hop of engine 4 (LL cell store -> the neighbour's poll sees it), measured in isolation
+# (tools/hop_bench.cu, profiles/r02/hop_latency_microbench.txt)
+HOP_US = 0.70
+
+
+def exchange_floor(st, ei, nt, t_newton):
+    """Engine 4's latency floor: every level solve of a warp group is a chain of 2 S dependent neighbour exchanges
+    (one per half-sweep); a group runs passes x nt levels one after another, so the solve cannot beat
+    levels_per_group x 2 S hops at the isolated hop latency."""
+    if ei.get("engine") != 4:
+        return None
+    levels = st["steps"]                      # levels processed by one warp group (passes x nt)
+    hops = levels * 2 * ei["sweeps"]
+    ms = hops * HOP_US * 1e-3
+    return {"levels_per_group": levels, "hops_on_chain": hops, "us_per_hop_isolated": HOP_US, "ms": ms,
+            "frac_of_solve": ms / (t_newton * 1e3), "source": "tools/hop_bench.cu (profiles/r02/hop_latency_microbench.txt)"}
 
 
 def sync_floor(st, nit, t_newton):
     """The latency floor of the persistent on-chip engines: the grid barriers the kernel counted (a wavefront step
     with i BiCGSTAB iterations costs 2 i + 1, or 2 i with the merged first iteration, plus one norm
     barrier per Newton iteration); at the isolated barrier cost they take `ms` of the solve's `t_newton`."""
-    if st.get("engine", 0) < 2:
+    if st.get("engine", 0) not in (2, 3):
         return None
     n = st.get("grid_barriers") or 2 * st["inner_iterations"] + st["steps"] + nit
     ms = n * BARRIER_US * 1e-3
@@ -182,6 +222,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-guess-run", action="store_true", help="skip the coarse-guess time-to-solution run")
     args = ap.parse_args()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        return relaunch_under_torchrun(args.gpus)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
 
@@ -227,6 +273,7 @@ def main():
         barrier()
     elapsed_ms = e0.elapsed_time(e1)
     nit, status = (int(v) for v in d_info.cpu())
+    ei = s.engine_info()
     elapsed_ms = max_over_ranks(elapsed_ms, dev)
     ms_per_step = elapsed_ms / args.steps
     dof_it = float(p.dof) * nit
@@ -305,13 +352,21 @@ def main():
                    "newton_iterations": nit, "status": status, "pipeline_depth": st["depth"], "grid_ctas": st["grid"],
                    "l2": f"inputs larger than L2 (U = {p.dof * 8 / 1e9:.2f} GB per iterate buffer)",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": "k_newton (persistent: a+b+c+d fused)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": ("k_newton_nb (engine 4, persistent: a+b+c+d fused)" if ei["engine"] == 4
+                                                else "k_newton_col (engine 3, persistent: a+b+c+d fused)"), "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "algorithmic": f"{BYTES_PER_DOF_IT} B per DOF per Newton iteration (SURVEY 8(d) fused minimum)"},
-        "kernels": {"k_newton_ms": t_newton * 1e3, "wavefront_steps": st["steps"],
-                    "bicgstab_iterations": st["inner_iterations"],
+        "kernels": {"k_newton_ms": t_newton * 1e3, "engine": ei["engine"],
+                    "level_solver": ({"method": "red-black SOR, fixed sweeps (engine 4)", "sweeps": ei["sweeps"],
+                                      "omega": ei["omega"], "jacobi_bound_q": ei["q"], "pipeline_depth": st["depth"],
+                                      "levels_per_group": st["steps"],
+                                      "rel_level_residual_per_newton_it": [r for r, _ in ei["linres"][:nit]]}
+                                     if ei["engine"] == 4 else
+                                     {"method": "Jacobi-scaled BiCGSTAB (engine 3)", "wavefront_steps": st["steps"],
+                                      "bicgstab_iterations": st["inner_iterations"]}),
                     "sync_floor": sync_floor(st, nit, t_newton),
+                    "exchange_floor": exchange_floor(st, ei, p.nt, t_newton),
                     "k_resjac": {"ms": resjac_ms, "GB/s": resjac_gbs, "frac": resjac_gbs / peak, "traffic": traffic_a,
                                  "algorithmic": f"{RESJAC_BYTES_PER_DOF} B/DOF",
                                  "kernel": "k_resjac_bulk (TMA-staged kernel a, all levels)"}},
@@ -325,7 +380,7 @@ def main():
         v, Lv, secs = oracle_sample(p, budget_s=args.ref_budget)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": f"sequential BDF1+Newton, levels 1..{Lv} of {p.nt} at full "
-                                          f"{p.nxu}x{p.nyu} (causal prefix), {secs:.1f} s single thread"}
+                                          f"{p.nxu}x{p.nyu} (causal prefix), {secs:.1f} s single thread", **cpu_info()}
     print(json.dumps(line), flush=True)
     s.close()
     if ws > 1:

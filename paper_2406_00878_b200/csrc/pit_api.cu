@@ -70,6 +70,7 @@ struct pit_handle {
     // engine 4 (neighbour-synchronised RB-SOR Newton solve, pit_newton_nb.cuh)
     bool nb = false;              // the Newton solve runs on engine 4
     int nb_rmax = 0, nb_G = 0, nb_D = 0, nb_dm = 0;   // base strip height, CTAs, iterations in flight, warp groups
+    int nb_threads = 0;                               // threads per CTA
     size_t nb_smem = 0;
     unsigned long long* nb_llx = nullptr;   // LL cells, x publications
     unsigned long long* nb_llu = nullptr;   // LL cells, U boundary-row publications
@@ -227,8 +228,8 @@ static const void* col_fn(int rmax, bool trace, int law, int nxu) {
 }
 
 // Engine 4 kernel for (base strip height, law, row length): its own translation units (pit_nb_law*.cu).
-static const void* nb_fn(int hb, int law, int nxu, int want_dm, size_t* smem, int* dm) {
-    return law == 1 ? nb_kernel_law1(hb, nxu, want_dm, smem, dm) : nb_kernel_law0(hb, nxu, want_dm, smem, dm);
+static const void* nb_fn(int hb, int law, int nxu, int want_dm, size_t* smem, int* dm, int* threads) {
+    return law == 1 ? nb_kernel_law1(hb, nxu, want_dm, smem, dm, threads) : nb_kernel_law0(hb, nxu, want_dm, smem, dm, threads);
 }
 
 // LAW 1 = viscous Burgers with constant viscosity (m2 = 0): specialised matvec coefficients.
@@ -393,13 +394,14 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
         const int G4 = std::min(h->sms, P.nyu);
         const int hb4 = P.nyu / G4;
         size_t smem4 = 0;
-        int occ4 = 0, dm = 1;
-        const void* fn = nb_fn(hb4, law, P.nxu, c.pipeline_depth, &smem4, &dm);
+        int occ4 = 0, dm = 1, thr4 = 0;
+        const void* fn = nb_fn(hb4, law, P.nxu, c.pipeline_depth, &smem4, &dm, &thr4);
         const int D4 = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : dm, std::min(dm, c.newton_max)));
         const int rmax = hb4;
         if (fn && smem4 <= 227 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4) == cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, fn, dm * (P.nxu / 2), smem4) == cudaSuccess && occ4 >= 1) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, fn, thr4, smem4) == cudaSuccess && occ4 >= 1) {
             h->nb = true; h->nb_rmax = rmax; h->nb_G = G4; h->nb_D = D4; h->nb_smem = smem4; h->nb_dm = dm;
+            h->nb_threads = thr4;
         }
         cudaGetLastError();
     }
@@ -586,10 +588,10 @@ static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, doub
     S.trace = h->trace ? h->trace + 13 : nullptr;
     void* args[] = {(void*)&S};
     size_t smem4 = 0;
-    int dm4 = 0;
-    const void* fn = nb_fn(h->nb_rmax, h->law, P.nxu, h->cfg.pipeline_depth, &smem4, &dm4);
+    int dm4 = 0, thr4 = 0;
+    const void* fn = nb_fn(h->nb_rmax, h->law, P.nxu, h->cfg.pipeline_depth, &smem4, &dm4, &thr4);
     CUDA_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->nb_smem));
-    CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->nb_G), dim3(h->nb_dm * (P.nxu / 2)), args, h->nb_smem, st));
+    CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->nb_G), dim3(h->nb_threads), args, h->nb_smem, st));
     CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
     h->launches += 9;
     h->last_engine = 4;

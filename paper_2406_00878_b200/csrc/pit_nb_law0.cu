@@ -3,23 +3,30 @@
 
 namespace pit {
 
-template <int HB, int NXU, int DM>
-static const void* nb_inst(size_t* smem, int* dm) {
-    *smem = NbEngine<HB, 0, NXU, DM>::SMEM;
+template <int HB, int NXU, int DM, int CPT>
+static const void* nb_inst(size_t* smem, int* dm, int* threads) {
+    *smem = NbEngine<HB, 0, NXU, DM, CPT>::SMEM;
     *dm = DM;
-    return (const void*)k_newton_nb<HB, 0, NXU, DM>;
+    *threads = DM * (NXU / CPT);
+    return (const void*)k_newton_nb<HB, 0, NXU, DM, CPT>;
 }
 
-// warp groups: DM * NXU / 2 <= 1024 threads; rows of 512: 2 groups by default, 3 on request (pipeline_depth 3)
-const void* nb_kernel_law0(int hb, int nxu, int want_dm, size_t* smem, int* dm) {
+// Instantiated shapes: (row length, base strip height HB) -> warp groups DM (Newton iterations in flight) and columns
+// per thread CPT = 2.  Rows of 512: 2 groups (768 threads at 3 groups cap registers at 80 and spill in the sweeps;
+// 4 columns per thread was slower everywhere); want_dm = 3 asks for the 3-group build.
+const void* nb_kernel_law0(int hb, int nxu, int want_dm, size_t* smem, int* dm, int* threads) {
     switch (nxu) {
-        case 64: return hb == 1 ? nb_inst<1, 64, 4>(smem, dm) : nullptr;
-        case 128: return hb == 1 ? nb_inst<1, 128, 4>(smem, dm) : nullptr;
-        case 256: return hb == 1 ? nb_inst<1, 256, 4>(smem, dm) : (hb == 2 ? nb_inst<2, 256, 4>(smem, dm) : nullptr);
+        case 64: return hb == 1 ? nb_inst<1, 64, 4, 2>(smem, dm, threads) : nullptr;
+        case 128: return hb == 1 ? nb_inst<1, 128, 4, 2>(smem, dm, threads) : nullptr;
+        case 256:
+            return hb == 1 ? nb_inst<1, 256, 4, 2>(smem, dm, threads)
+                           : (hb == 2 ? nb_inst<2, 256, 4, 2>(smem, dm, threads) : nullptr);
         case 512:
-            if (want_dm != 3)   // default: 2 groups (128 registers; the 3-group build spills)
-                return hb == 1 ? nb_inst<1, 512, 2>(smem, dm) : (hb == 2 ? nb_inst<2, 512, 2>(smem, dm) : (hb == 3 ? nb_inst<3, 512, 2>(smem, dm) : nullptr));
-            return hb == 1 ? nb_inst<1, 512, 3>(smem, dm) : (hb == 2 ? nb_inst<2, 512, 3>(smem, dm) : (hb == 3 ? nb_inst<3, 512, 3>(smem, dm) : nullptr));
+            if (want_dm == 3)
+                return hb == 1 ? nb_inst<1, 512, 3, 2>(smem, dm, threads)
+                               : (hb == 2 ? nb_inst<2, 512, 3, 2>(smem, dm, threads) : (hb == 3 ? nb_inst<3, 512, 3, 2>(smem, dm, threads) : nullptr));
+            return hb == 1 ? nb_inst<1, 512, 2, 2>(smem, dm, threads)
+                           : (hb == 2 ? nb_inst<2, 512, 2, 2>(smem, dm, threads) : (hb == 3 ? nb_inst<3, 512, 2, 2>(smem, dm, threads) : nullptr));
         default: return nullptr;
     }
 }

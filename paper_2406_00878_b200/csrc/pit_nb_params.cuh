@@ -20,7 +20,7 @@ struct NbParams {
     double* U;                  // [B][nt][ns] iterate ring (iterate k in buffer k % B), buffer 0 = U_0
     int B, D, G;
     const double* ctl;          // [4] = { omega, sweeps, q, check stride } written on the device by k_nb_ctl
-    unsigned long long* llx;    // [G][DM][NB_RX][2 sides][T] cells (2 words each)
+    unsigned long long* llx;    // [G][DM][NB_RX][2 sides][NXU / 2] cells (2 words each)
     unsigned long long* llu;    // [G][DM][NB_RU][2 sides][NXU] cells
     double* hpart;              // [MAXK][G][NB_NP]
     unsigned* arrive;           // [MAXK] CTAs done with iteration k
@@ -39,8 +39,8 @@ constexpr int NB_TR = 8;        // trace: prologue, sweeps, sweep waits, epilogu
 // Implemented in pit_nb_law{0,1}.cu: the engine-4 kernel for (base strip height hb, row length nxu), its dynamic
 // shared memory and its warp groups (iterations in flight; want_dm = 2 asks for the 2-group build where one
 // exists); nullptr if that shape has no instantiation.
-const void* nb_kernel_law0(int hb, int nxu, int want_dm, size_t* smem, int* dm);
-const void* nb_kernel_law1(int hb, int nxu, int want_dm, size_t* smem, int* dm);
+const void* nb_kernel_law0(int hb, int nxu, int want_dm, size_t* smem, int* dm, int* threads);
+const void* nb_kernel_law1(int hb, int nxu, int want_dm, size_t* smem, int* dm, int* threads);
 // omega and the sweep count on the device (k_nb_q + k_nb_ctl, pit_newton_nb.cuh) on stream st
 void nb_setup_launch(const Prob& P, const double* U1, const double* ring, unsigned long long* qbits, double lin_rtol,
                      int sweeps, int check, double* ctl, int grid, cudaStream_t st);

@@ -38,6 +38,10 @@ __device__ __forceinline__ void ll_put(unsigned long long* p, double v, unsigned
     const unsigned long long w1 = ((unsigned long long)f << 32) | (unsigned)__double2hiint(v);
     asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
 }
+// The poll is a strong GPU-scope load (each 8-byte word single-copy atomic; data and flag share a word).  One hop
+// (store -> the neighbour's poll sees it) costs ~0.7 us on B200 whatever the store flavour (tools/hop_bench.cu,
+// profiles/r02/hop_latency_microbench.txt).  ld.global.cv / .cg polls look twice as fast there but return words whose
+// data does not belong to the flag they carry (tools/ll_check.cu, profiles/r02/ll_poll_correctness.txt): not usable.
 __device__ __forceinline__ LLc ll_issue(const unsigned long long* p) {
     LLc c;
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(c.w0), "=l"(c.w1) : "l"(p) : "memory");
@@ -91,29 +95,32 @@ static __global__ void k_nb_ctl(const unsigned long long* qbits, double lin_rtol
 
 
 // ---- the persistent kernel ------------------------------------------------------------------------------------
-// Storage is COLOUR-indexed: v[r][0] is the red point of own row r (column 2t + ((r0 + r) & 1)), v[r][1] the black
-// one.  The strip height H and the parity PR0 of the first own row are template parameters of the body (every CTA
-// has H in {HB, HB + 1}), so every sweep indexes registers with compile-time subscripts, has no row guards, and knows
-// at compile time which column of its pair a colour occupies (the sign of the in-thread E/W coefficient and the
-// shared-memory slot of the out-of-thread neighbour).
-template <int HB, int LAW, int NXU, int DM>
+// Thread t of a group owns CPT consecutive columns CPT t .. CPT t + CPT - 1 of the strip's rows (registers, physical
+// order).  The strip height H and the parity PR0 of the first own row are template parameters of the body (every
+// CTA has H in {HB, HB + 1}), so the colour of every register, the in-thread / out-of-thread split of the E/W
+// neighbours and every subscript are compile-time: no row guards, no selects, no dynamic indexing.  A colour has
+// HC = CPT / 2 points per thread and row; the h-th is column ((PR0 + r + colour) & 1) + 2h.
+template <int HB, int LAW, int NXU, int DM, int CPT>
 struct NbEngine {
-    static constexpr int T = NXU / 2;          // threads per group
+    static constexpr int T = NXU / CPT;        // threads per group
     static constexpr int NT = DM * T;          // threads per CTA
     static constexpr int W = NXU + 2;          // smem row pitch: column i at i + 1, pads at 0 and NXU + 1
     static constexpr int NW = T / 32;          // warps per group
     static constexpr int RM = HB + 1;          // max strip height
+    static constexpr int HC = CPT / 2;         // points of one colour per thread and row
     static constexpr size_t OFF_Q = 0;                                   // qs  [DM][RM][W]  sweep exchange values
     static constexpr size_t OFF_U = OFF_Q + (size_t)DM * RM * W;         // us  [DM][RM][W]  staged u rows
-    static constexpr size_t OFF_B = OFF_U + (size_t)DM * RM * W;         // bs  [DM][RM][2][T] right-hand sides
-    static constexpr size_t OFF_A = OFF_B + (size_t)DM * RM * 2 * T;     // acc [DM][NB_NP][T]
+    static constexpr size_t OFF_B = OFF_U + (size_t)DM * RM * W;         // bs  [DM][RM][CPT][T] right-hand sides
+    static constexpr size_t OFF_A = OFF_B + (size_t)DM * RM * CPT * T;   // acc [DM][NB_NP][T]
     static constexpr size_t SMEM = (OFF_A + (size_t)DM * NB_NP * T) * sizeof(double);
+    static_assert(NW >= 1 && T % 32 == 0, "a group is whole warps");
 
     template <int H, int PR0>
     __device__ __forceinline__ static void run(const NbParams& S, double* sm) {
         const Prob P = S.P;
         const int G = S.G, c = blockIdx.x;
-        const int p = threadIdx.x / T, t = threadIdx.x % T;   // warp group (pipeline slot), column pair
+        const int p = threadIdx.x / T, t = threadIdx.x % T;   // warp group (Newton iteration in flight), columns
+        const int c0 = CPT * t;                                // first own column
         const long long ns = P.ns;
         const int nyu = P.nyu, nt = P.nt, D = S.D, B = S.B;
         const bool per = P.bc == 1;
@@ -123,27 +130,25 @@ struct NbEngine {
         const int cn = c + 1 < G ? c + 1 : (per ? 0 : -1);  // north neighbour strip
         const double omega = __ldcg(S.ctl), tau = P.dt;
         const int SW = (int)__ldcg(S.ctl + 1);
-        const int chk = max(1, (int)__ldcg(S.ctl + 3));      // red-residual check stride (levels)
+        const int chk = max(1, (int)__ldcg(S.ctl + 3));      // level-residual check stride (levels)
         const int nxp = P.nx + 1;
         // LAW 1 (Burgers, constant mu = m0): a_E x_E = x_E (ax u_E - bx), a_W x_W = x_W (-ax u_W - bx), same in y
         const double ax = tau * P.i2hx, bx = tau * P.m0 * P.ihx2, ay = tau * P.i2hy, by = tau * P.m0 * P.ihy2;
         const double aC1 = 1.0 + 2.0 * (bx + by), invC1 = 1.0 / aC1;
         const double rfac = (1.0 - omega) / omega;
-        constexpr int PRH = (PR0 + H - 1) & 1;   // parity of the top own row
 
         double* qs = sm + OFF_Q + (size_t)p * RM * W;          // this group's arrays
         double* us = sm + OFF_U + (size_t)p * RM * W;
-        double* bs = sm + OFF_B + (size_t)p * RM * 2 * T;
+        double* bs = sm + OFF_B + (size_t)p * RM * CPT * T;
         double* acc = sm + OFF_A + (size_t)p * NB_NP * T;
         __shared__ double red_s[DM][NW][NB_NP];
         __shared__ int s_dec[2];
         __shared__ int s_last[DM];
         __shared__ volatile int lvl_done[DM];    // levels of the current pass each group has finished
 
-        // group state in registers (row and colour subscripts compile-time)
-        double x[H][2], u[H][2];
-        double uS[2], uN[2];                     // halo rows in the colour frame of own row 0 / own row H-1
-        double co[LAW == 0 ? H : 1][2][5];       // LAW 0: 1/a_C, a_E, a_W, a_N, a_S
+        double x[H][CPT], u[H][CPT];
+        double hS[CPT], hN[CPT];                 // u of the halo rows r0 - 1 and r0 + H (physical columns)
+        double co[LAW == 0 ? H : 1][LAW == 0 ? CPT : 1][5];   // LAW 0: 1/a_C, a_E, a_W, a_N, a_S
         int lastx = -1;
         unsigned qx = 0, qu = 0;                 // publication counters of this group (identical in every CTA)
         long long levels = 0;
@@ -159,8 +164,8 @@ struct NbEngine {
         auto ring_left = [&](const double* rg, int j) { return rg ? __ldcg(rg + 2 * nxp + j) : 0.0; };
         auto ring_right = [&](const double* rg, int j) { return rg ? __ldcg(rg + 2 * nxp + (P.ny - 1) + j) : 0.0; };
 
-        // LL channels of group p: x ring [G][DM][NB_RX][2][T], U ring [G][DM][NB_RU][2][NXU] (2 words per cell)
-        auto xbase = [&](int cta) { return S.llx + (((size_t)cta * DM + p) * NB_RX * 2 * T) * 2; };
+        // LL channels of group p: x ring [G][DM][NB_RX][2][HC][T], U ring [G][DM][NB_RU][2][NXU] (2 words per cell)
+        auto xbase = [&](int cta) { return S.llx + (((size_t)cta * DM + p) * NB_RX * 2 * HC * T) * 2; };
         auto ubase = [&](int cta, int grp) { return S.llu + (((size_t)cta * DM + grp) * NB_RU * 2 * NXU) * 2; };
         unsigned long long* myx = xbase(c);
         unsigned long long* myu = ubase(c, p);
@@ -168,12 +173,25 @@ struct NbEngine {
         const unsigned long long* nxq = cn >= 0 ? xbase(cn) : nullptr;
         const unsigned long long* su = (cs >= 0 && p > 0) ? ubase(cs, p - 1) : nullptr;   // U_k^n of their group p-1
         const unsigned long long* nu = (cn >= 0 && p > 0) ? ubase(cn, p - 1) : nullptr;
-        auto xcell = [&](auto* base, unsigned q, int side) { return base + ((size_t)((q % NB_RX) * 2 + side) * T + t) * 2; };
-        auto ucell = [&](auto* base, unsigned q, int side, int col) {
-            return base + ((size_t)((q % NB_RU) * 2 + side) * NXU + 2 * t + col) * 2;
+        auto xcell = [&](auto* base, unsigned q, int side, int h) {
+            return base + ((size_t)(((q % NB_RX) * 2 + side) * HC + h) * T + t) * 2;
         };
-        auto bsm = [&](int r, int cl) -> double& { return bs[(size_t)(r * 2 + cl) * T + t]; };
+        auto ucell = [&](auto* base, unsigned q, int side, int j) {
+            return base + ((size_t)((q % NB_RU) * 2 + side) * NXU + c0 + j) * 2;
+        };
+        auto bsm = [&](int r, int j) -> double& { return bs[(size_t)(r * CPT + j) * T + t]; };
         auto ac = [&](int j) -> double& { return acc[(size_t)j * T + t]; };
+        // exchange value of column j of row r for the neighbouring thread (LAW 1: premultiplied by the coefficient
+        // the neighbour applies: column c0 is the E neighbour of c0 - 1, column c0 + CPT - 1 the W neighbour of c0 + CPT)
+        auto put_q = [&](double* q, int r, int j, double xv, double uv) {
+            double v = xv;
+            if (LAW == 1) v *= j == 0 ? fma(ax, uv, -bx) : fma(-ax, uv, -bx);
+            q[r * W + c0 + j + 1] = v;
+            if (per) {
+                if (j == 0 && t == 0) q[r * W + NXU + 1] = v;
+                if (j == CPT - 1 && t == T - 1) q[r * W + 0] = v;
+            }
+        };
 
         for (int i = t; i < NB_NP * T; i += T) acc[i] = 0.0;
         for (int i = t; i < RM * W; i += T) { qs[i] = 0.0; us[i] = 0.0; }
@@ -184,7 +202,9 @@ struct NbEngine {
             const int k = pass * D + p;
             const bool active = p < D && k < S.newton_max;
             #pragma unroll
-            for (int r = 0; r < H; ++r) x[r][0] = x[r][1] = 0.0;   // carry du^0 = 0
+            for (int r = 0; r < H; ++r)
+                #pragma unroll
+                for (int j = 0; j < CPT; ++j) x[r][j] = 0.0;   // carry du^0 = 0
             lastx = -1;
             for (int n = 1; active && n <= nt; ++n) {
                 ++levels;
@@ -202,19 +222,21 @@ struct NbEngine {
                 const double* up = n == 1 ? S.u0 : Uk + (size_t)(n - 2) * ns;
                 const double* rg = S.ring ? S.ring + (size_t)(n - 1) * P.ring_len : nullptr;
                 // ---- prologue A: u^n own rows (+ staging), halo rows, u^{n-1} own rows
-                double2 pv[H];
+                double pv[H][CPT];
                 #pragma unroll
                 for (int r = 0; r < H; ++r) {
-                    const double2 v = *reinterpret_cast<const double2*>(un + (size_t)(r0 + r) * NXU + 2 * t);
-                    pv[r] = *reinterpret_cast<const double2*>(up + (size_t)(r0 + r) * NXU + 2 * t);
-                    const int pr = (PR0 ^ r) & 1;
-                    u[r][0] = pr ? v.y : v.x;
-                    u[r][1] = pr ? v.x : v.y;
-                    us[r * W + 2 * t + 1] = v.x;
-                    us[r * W + 2 * t + 2] = v.y;
+                    #pragma unroll
+                    for (int j = 0; j < CPT; j += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(un + (size_t)(r0 + r) * NXU + c0 + j);
+                        const double2 w = *reinterpret_cast<const double2*>(up + (size_t)(r0 + r) * NXU + c0 + j);
+                        u[r][j] = v.x; u[r][j + 1] = v.y;
+                        pv[r][j] = w.x; pv[r][j + 1] = w.y;
+                        us[r * W + c0 + j + 1] = v.x;
+                        us[r * W + c0 + j + 2] = v.y;
+                    }
                     if (per) {
-                        if (t == 0) us[r * W + NXU + 1] = v.x;
-                        if (t == T - 1) us[r * W + 0] = v.y;
+                        if (t == 0) us[r * W + NXU + 1] = u[r][0];
+                        if (t == T - 1) us[r * W + 0] = u[r][CPT - 1];
                     } else {
                         if (t == 0) us[r * W + 0] = ring_left(rg, r0 + r);
                         if (t == T - 1) us[r * W + NXU + 1] = ring_right(rg, r0 + r);
@@ -225,65 +247,57 @@ struct NbEngine {
                 #pragma unroll
                 for (int side = 0; side < 2; ++side) {
                     const int nb = side ? cn : cs;
-                    double v0, v1;   // physical columns 2t, 2t+1
+                    double* dst = side ? hN : hS;
                     if (nb < 0) {    // Dirichlet boundary row
-                        v0 = side ? ring_top(rg, 2 * t) : ring_bottom(rg, 2 * t);
-                        v1 = side ? ring_top(rg, 2 * t + 1) : ring_bottom(rg, 2 * t + 1);
+                        #pragma unroll
+                        for (int j = 0; j < CPT; ++j) dst[j] = side ? ring_top(rg, c0 + j) : ring_bottom(rg, c0 + j);
                     } else if (p == 0) {
-                        const int j = side ? (r0 + H) % nyu : (r0 - 1 + nyu) % nyu;
-                        const double2 v = ldcg2(un + (size_t)j * NXU + 2 * t);
-                        v0 = v.x; v1 = v.y;
+                        const int jr = side ? (r0 + H) % nyu : (r0 - 1 + nyu) % nyu;
+                        #pragma unroll
+                        for (int j = 0; j < CPT; j += 2) {
+                            const double2 v = ldcg2(un + (size_t)jr * NXU + c0 + j);
+                            dst[j] = v.x; dst[j + 1] = v.y;
+                        }
                     } else {
                         const unsigned qn = (unsigned)(pass * nt + n - 1);   // group p-1 publishes U once per level
                         const unsigned long long* base = side ? nu : su;
                         const int sd = side ? 0 : 1;    // north strip's bottom row / south strip's top row
-                        const LLc a0 = ll_issue(ucell(base, qn, sd, 0));
-                        const LLc a1 = ll_issue(ucell(base, qn, sd, 1));
-                        v0 = ll_take_t(ucell(base, qn, sd, 0), a0, qn + 1u, tr[2]);
-                        v1 = ll_take_t(ucell(base, qn, sd, 1), a1, qn + 1u, tr[2]);
+                        LLc a[CPT];
+                        #pragma unroll
+                        for (int j = 0; j < CPT; ++j) a[j] = ll_issue(ucell(base, qn, sd, j));
+                        #pragma unroll
+                        for (int j = 0; j < CPT; ++j) dst[j] = ll_take_t(ucell(base, qn, sd, j), a[j], qn + 1u, tr[2]);
                     }
-                    const int pr = side ? PRH : PR0;
-                    double* dst = side ? uN : uS;
-                    dst[0] = pr ? v1 : v0;
-                    dst[1] = pr ? v0 : v1;
                 }
                 gbar();
-                // ---- prologue B: residual r^n = -G^n, b = r^n + du^{n-1}, sweep values of x0
+                // ---- prologue B: residual r^n = -G^n, b = r^n + du^{n-1}, exchange values of x0
                 {
                     double ar2 = 0.0, arm = 0.0;
                     #pragma unroll
                     for (int r = 0; r < H; ++r) {
                         #pragma unroll
-                        for (int cl = 0; cl < 2; ++cl) {
-                            const int phys = (PR0 ^ r ^ cl) & 1;   // 0: column 2t (E neighbour in-thread), 1: 2t+1
+                        for (int j = 0; j < CPT; ++j) {
                             Vals v;
-                            v.c = u[r][cl];
-                            v.e = phys == 0 ? u[r][cl ^ 1] : us[r * W + 2 * t + 3];
-                            v.w = phys == 1 ? u[r][cl ^ 1] : us[r * W + 2 * t];
-                            v.n = r + 1 < H ? u[r + 1 < H ? r + 1 : r][cl ^ 1] : uN[cl];
-                            v.s = r > 0 ? u[r > 0 ? r - 1 : 0][cl ^ 1] : uS[cl];
-                            const double upv = phys ? pv[r].y : pv[r].x;
+                            v.c = u[r][j];
+                            v.e = j + 1 < CPT ? u[r][j + 1 < CPT ? j + 1 : j] : us[r * W + c0 + CPT + 1];
+                            v.w = j > 0 ? u[r][j > 0 ? j - 1 : 0] : us[r * W + c0];
+                            v.n = r + 1 < H ? u[r + 1 < H ? r + 1 : r][j] : hN[j];
+                            v.s = r > 0 ? u[r > 0 ? r - 1 : 0][j] : hS[j];
                             double G_;
                             if (LAW == 1) {
                                 const double conv = 0.5 * ((v.e * v.e - v.w * v.w) * P.i2hx + (v.n * v.n - v.s * v.s) * P.i2hy);
                                 const double visc = P.m0 * ((v.e - 2.0 * v.c + v.w) * P.ihx2 + (v.n - 2.0 * v.c + v.s) * P.ihy2);
-                                G_ = (v.c - upv) + tau * (conv - visc);
+                                G_ = (v.c - pv[r][j]) + tau * (conv - visc);
                             } else {
-                                const RJ o = residual_jacobian_raw(P, v, upv);
+                                const RJ o = residual_jacobian_raw(P, v, pv[r][j]);
                                 G_ = o.G;
-                                double* cf = co[LAW == 0 ? r : 0][cl];
+                                double* cf = co[LAW == 0 ? r : 0][LAW == 0 ? j : 0];
                                 cf[0] = 1.0 / o.aC; cf[1] = o.aE; cf[2] = o.aW; cf[3] = o.aN; cf[4] = o.aS;
                             }
-                            bsm(r, cl) = x[r][cl] - G_;      // b = r^n + du^{n-1}, r^n = -G^n
+                            bsm(r, j) = x[r][j] - G_;      // b = r^n + du^{n-1}, r^n = -G^n
                             ar2 = fma(G_, G_, ar2);
                             arm = fmax(arm, fabs(G_));
-                            double qv = x[r][cl];          // the sweeps' exchange value of x0 at this column
-                            if (LAW == 1) qv *= phys ? fma(-ax, v.c, -bx) : fma(ax, v.c, -bx);
-                            qs[r * W + 2 * t + 1 + phys] = qv;
-                            if (per) {
-                                if (t == 0 && phys == 0) qs[r * W + NXU + 1] = qv;
-                                if (t == T - 1 && phys == 1) qs[r * W + 0] = qv;
-                            }
+                            if (j == 0 || j == CPT - 1) put_q(qs, r, j, x[r][j], v.c);
                         }
                     }
                     ac(0) += ar2;
@@ -297,72 +311,75 @@ struct NbEngine {
                     const bool lastm = m == SW - 1 && chkl;
                     #pragma unroll
                     for (int cc = 0; cc < 2; ++cc) {
-                        double xs_h = 0.0, xn_h = 0.0;
+                        double xs_h[HC], xn_h[HC];
+                        #pragma unroll
+                        for (int h = 0; h < HC; ++h) xs_h[h] = xn_h[h] = 0.0;
                         if (lastx >= 0) {
                             const unsigned qn = (unsigned)lastx;
-                            LLc hs, hn;
-                            if (cs >= 0) hs = ll_issue(xcell(sx, qn, 1));
-                            if (cn >= 0) hn = ll_issue(xcell(nxq, qn, 0));
-                            if (cs >= 0) xs_h = ll_take_t(xcell(sx, qn, 1), hs, qn + 1u, tr[2]);
-                            if (cn >= 0) xn_h = ll_take_t(xcell(nxq, qn, 0), hn, qn + 1u, tr[2]);
+                            LLc hs[HC], hn[HC];
+                            #pragma unroll
+                            for (int h = 0; h < HC; ++h) {
+                                if (cs >= 0) hs[h] = ll_issue(xcell(sx, qn, 1, h));
+                                if (cn >= 0) hn[h] = ll_issue(xcell(nxq, qn, 0, h));
+                            }
+                            #pragma unroll
+                            for (int h = 0; h < HC; ++h) {
+                                if (cs >= 0) xs_h[h] = ll_take_t(xcell(sx, qn, 1, h), hs[h], qn + 1u, tr[2]);
+                                if (cn >= 0) xn_h[h] = ll_take_t(xcell(nxq, qn, 0, h), hn[h], qn + 1u, tr[2]);
+                            }
                         }
                         double rs2 = 0.0, rsm = 0.0;
                         // boundary rows first and published at once (the neighbours wait for them), then the interior
                         #pragma unroll
                         for (int i = 0; i < H; ++i) {
                             const int r = i == 0 ? 0 : (i == 1 ? H - 1 : i - 1);
-                            const int phys = (PR0 ^ r ^ cc) & 1;   // compile-time after unrolling
-                            const double xo = x[r][cc];
-                            const double xI = x[r][cc ^ 1];
-                            const double qR = qs[r * W + (phys ? 2 * t + 3 : 2 * t)];
-                            const double xN = r + 1 < H ? x[r + 1 < H ? r + 1 : r][cc ^ 1] : xn_h;
-                            const double xS = r > 0 ? x[r > 0 ? r - 1 : 0][cc ^ 1] : xs_h;
-                            const double bb = bsm(r, cc);
-                            double xn, dC;
-                            if (LAW == 1) {
-                                const double uI = u[r][cc ^ 1];
-                                const double uNv = r + 1 < H ? u[r + 1 < H ? r + 1 : r][cc ^ 1] : uN[cc];
-                                const double uSv = r > 0 ? u[r > 0 ? r - 1 : 0][cc ^ 1] : uS[cc];
-                                const double cI = phys ? fma(-ax, uI, -bx) : fma(ax, uI, -bx);   // in-thread W / E
-                                double tt = bb - qR;
-                                tt = fma(-cI, xI, tt);
-                                tt = fma(-fma(ay, uNv, -by), xN, tt);
-                                tt = fma(-fma(-ay, uSv, -by), xS, tt);
-                                xn = fma(omega, fma(tt, invC1, -xo), xo);
-                                dC = aC1;
-                                const double uc = u[r][cc];
-                                const double qv = xn * (phys ? fma(-ax, uc, -bx) : fma(ax, uc, -bx));
-                                qs[r * W + 2 * t + 1 + phys] = qv;
-                                if (per) {
-                                    if (phys == 0 && t == 0) qs[r * W + NXU + 1] = qv;
-                                    if (phys == 1 && t == T - 1) qs[r * W + 0] = qv;
+                            #pragma unroll
+                            for (int h = 0; h < HC; ++h) {
+                                const int j = ((PR0 + r + cc) & 1) + 2 * h;   // compile-time after unrolling
+                                const double xo = x[r][j];
+                                const double xN = r + 1 < H ? x[r + 1 < H ? r + 1 : r][j] : xn_h[h];
+                                const double xS = r > 0 ? x[r > 0 ? r - 1 : 0][j] : xs_h[h];
+                                const double bb = bsm(r, j);
+                                double xn, dC;
+                                if (LAW == 1) {
+                                    double tt = bb;
+                                    if (j + 1 < CPT) tt = fma(-fma(ax, u[r][j + 1 < CPT ? j + 1 : j], -bx), x[r][j + 1 < CPT ? j + 1 : j], tt);
+                                    else tt -= qs[r * W + c0 + CPT + 1];
+                                    if (j > 0) tt = fma(-fma(-ax, u[r][j > 0 ? j - 1 : 0], -bx), x[r][j > 0 ? j - 1 : 0], tt);
+                                    else tt -= qs[r * W + c0];
+                                    const double uNv = r + 1 < H ? u[r + 1 < H ? r + 1 : r][j] : hN[j];
+                                    const double uSv = r > 0 ? u[r > 0 ? r - 1 : 0][j] : hS[j];
+                                    tt = fma(-fma(ay, uNv, -by), xN, tt);
+                                    tt = fma(-fma(-ay, uSv, -by), xS, tt);
+                                    xn = fma(omega, fma(tt, invC1, -xo), xo);
+                                    dC = aC1;
+                                } else {
+                                    const double* cf = co[LAW == 0 ? r : 0][LAW == 0 ? j : 0];
+                                    const double xE = j + 1 < CPT ? x[r][j + 1 < CPT ? j + 1 : j] : qs[r * W + c0 + CPT + 1];
+                                    const double xW = j > 0 ? x[r][j > 0 ? j - 1 : 0] : qs[r * W + c0];
+                                    double tt = bb;
+                                    tt = fma(-cf[1], xE, tt);
+                                    tt = fma(-cf[2], xW, tt);
+                                    tt = fma(-cf[3], xN, tt);
+                                    tt = fma(-cf[4], xS, tt);
+                                    xn = fma(omega, fma(tt, cf[0], -xo), xo);
+                                    dC = 1.0 / cf[0];
                                 }
-                            } else {
-                                const double* cf = co[LAW == 0 ? r : 0][cc];
-                                const double aI = phys ? cf[2] : cf[1], aR = phys ? cf[1] : cf[2];
-                                double tt = bb;
-                                tt = fma(-aR, qR, tt);
-                                tt = fma(-aI, xI, tt);
-                                tt = fma(-cf[3], xN, tt);
-                                tt = fma(-cf[4], xS, tt);
-                                xn = fma(omega, fma(tt, cf[0], -xo), xo);
-                                dC = 1.0 / cf[0];
-                                qs[r * W + 2 * t + 1 + phys] = xn;
-                                if (per) {
-                                    if (phys == 0 && t == 0) qs[r * W + NXU + 1] = xn;
-                                    if (phys == 1 && t == T - 1) qs[r * W + 0] = xn;
+                                x[r][j] = xn;
+                                if (j == 0 || j == CPT - 1) put_q(qs, r, j, xn, u[r][j]);
+                                if (cc == 1 && lastm) {   // residual of a just-updated black point
+                                    const double rr = dC * rfac * (xn - xo);
+                                    rs2 = fma(rr, rr, rs2);
+                                    rsm = fmax(rsm, fabs(rr));
                                 }
                             }
-                            x[r][cc] = xn;
-                            if (cc == 1 && lastm) {   // residual of a just-updated black point
-                                const double rr = dC * rfac * (xn - xo);
-                                rs2 = fma(rr, rr, rs2);
-                                rsm = fmax(rsm, fabs(rr));
-                            }
-                            if (i == (H > 1 ? 1 : 0)) {   // this colour's boundary values: side 0 own row 0, side 1 row H-1
+                            if (i == (H > 1 ? 1 : 0)) {   // this colour's boundary values: side 0 row 0, side 1 row H-1
                                 const unsigned f = qx + 1u;
-                                if (cs >= 0) ll_put(xcell(myx, qx, 0), x[0][cc], f);
-                                if (cn >= 0) ll_put(xcell(myx, qx, 1), x[H - 1][cc], f);
+                                #pragma unroll
+                                for (int h = 0; h < HC; ++h) {
+                                    if (cs >= 0) ll_put(xcell(myx, qx, 0, h), x[0][((PR0 + cc) & 1) + 2 * h], f);
+                                    if (cn >= 0) ll_put(xcell(myx, qx, 1, h), x[H - 1][((PR0 + H - 1 + cc) & 1) + 2 * h], f);
+                                }
                             }
                         }
                         if (cc == 1 && lastm) {
@@ -381,21 +398,22 @@ struct NbEngine {
                     double d2 = 0.0, dm = 0.0;
                     #pragma unroll
                     for (int r = 0; r < H; ++r) {
-                        const int pr = (PR0 ^ r) & 1;
-                        const double w0 = u[r][0] + x[r][0], w1 = u[r][1] + x[r][1];   // red, black
-                        double2 v;
-                        v.x = pr ? w1 : w0;
-                        v.y = pr ? w0 : w1;
-                        *reinterpret_cast<double2*>(Un + (size_t)(r0 + r) * NXU + 2 * t) = v;
-                        d2 = fma(x[r][0], x[r][0], fma(x[r][1], x[r][1], d2));
-                        dm = fmax(dm, fmax(fabs(x[r][0]), fabs(x[r][1])));
-                        if (r == 0 && cs >= 0) {
-                            ll_put(ucell(myu, qu, 0, 0), v.x, qu + 1u);
-                            ll_put(ucell(myu, qu, 0, 1), v.y, qu + 1u);
-                        }
-                        if (r == H - 1 && cn >= 0) {
-                            ll_put(ucell(myu, qu, 1, 0), v.x, qu + 1u);
-                            ll_put(ucell(myu, qu, 1, 1), v.y, qu + 1u);
+                        #pragma unroll
+                        for (int j = 0; j < CPT; j += 2) {
+                            double2 v;
+                            v.x = u[r][j] + x[r][j];
+                            v.y = u[r][j + 1] + x[r][j + 1];
+                            *reinterpret_cast<double2*>(Un + (size_t)(r0 + r) * NXU + c0 + j) = v;
+                            d2 = fma(x[r][j], x[r][j], fma(x[r][j + 1], x[r][j + 1], d2));
+                            dm = fmax(dm, fmax(fabs(x[r][j]), fabs(x[r][j + 1])));
+                            if (r == 0 && cs >= 0) {
+                                ll_put(ucell(myu, qu, 0, j), v.x, qu + 1u);
+                                ll_put(ucell(myu, qu, 0, j + 1), v.y, qu + 1u);
+                            }
+                            if (r == H - 1 && cn >= 0) {
+                                ll_put(ucell(myu, qu, 1, j), v.x, qu + 1u);
+                                ll_put(ucell(myu, qu, 1, j + 1), v.y, qu + 1u);
+                            }
                         }
                     }
                     ++qu;
@@ -407,39 +425,45 @@ struct NbEngine {
                         lvl_done[p] = n;                  // group p+1 may start level n
                     }
                 }
-                // ---- a-posteriori residual of the red points after the final black half-sweep (every check-th
-                //      level: it waits for the neighbours' final black rows, one more exchange on this group's chain)
+                // ---- a-posteriori residual of the red points after the final black half-sweep (every chk-th level:
+                //      it waits for the neighbours' final black rows, one more exchange on this group's chain)
                 if (chkl) {
                     const unsigned qn = (unsigned)lastx;
-                    LLc hs, hn;
-                    if (cs >= 0) hs = ll_issue(xcell(sx, qn, 1));
-                    if (cn >= 0) hn = ll_issue(xcell(nxq, qn, 0));
-                    const double xs_h = cs >= 0 ? ll_take_t(xcell(sx, qn, 1), hs, qn + 1u, tr[2]) : 0.0;
-                    const double xn_h = cn >= 0 ? ll_take_t(xcell(nxq, qn, 0), hn, qn + 1u, tr[2]) : 0.0;
+                    double xs_h[HC], xn_h[HC];
+                    #pragma unroll
+                    for (int h = 0; h < HC; ++h) {
+                        xs_h[h] = cs >= 0 ? ll_take(xcell(sx, qn, 1, h), ll_issue(xcell(sx, qn, 1, h)), qn + 1u) : 0.0;
+                        xn_h[h] = cn >= 0 ? ll_take(xcell(nxq, qn, 0, h), ll_issue(xcell(nxq, qn, 0, h)), qn + 1u) : 0.0;
+                    }
                     double rs2 = 0.0, rsm = 0.0, bb2 = 0.0;
                     #pragma unroll
                     for (int r = 0; r < H; ++r) {
-                        const int phys = (PR0 ^ r) & 1;            // the red column of row r
-                        const double xo = x[r][0], xI = x[r][1];
-                        const double qR = qs[r * W + (phys ? 2 * t + 3 : 2 * t)];
-                        const double xN = r + 1 < H ? x[r + 1 < H ? r + 1 : r][1] : xn_h;
-                        const double xS = r > 0 ? x[r > 0 ? r - 1 : 0][1] : xs_h;
-                        const double b0 = bsm(r, 0), b1 = bsm(r, 1);
-                        double rr;
-                        if (LAW == 1) {
-                            const double uI = u[r][1];
-                            const double uNv = r + 1 < H ? u[r + 1 < H ? r + 1 : r][1] : uN[0];
-                            const double uSv = r > 0 ? u[r > 0 ? r - 1 : 0][1] : uS[0];
-                            const double cI = phys ? fma(-ax, uI, -bx) : fma(ax, uI, -bx);
-                            rr = b0 - qR - cI * xI - fma(ay, uNv, -by) * xN - fma(-ay, uSv, -by) * xS - aC1 * xo;
-                        } else {
-                            const double* cf = co[LAW == 0 ? r : 0][0];
-                            const double aI = phys ? cf[2] : cf[1], aR = phys ? cf[1] : cf[2];
-                            rr = b0 - aR * qR - aI * xI - cf[3] * xN - cf[4] * xS - xo / cf[0];
+                        #pragma unroll
+                        for (int h = 0; h < HC; ++h) {
+                            const int j = ((PR0 + r) & 1) + 2 * h;     // red points
+                            const double xo = x[r][j];
+                            const double xN = r + 1 < H ? x[r + 1 < H ? r + 1 : r][j] : xn_h[h];
+                            const double xS = r > 0 ? x[r > 0 ? r - 1 : 0][j] : xs_h[h];
+                            double rr = bsm(r, j);
+                            if (LAW == 1) {
+                                if (j + 1 < CPT) rr -= fma(ax, u[r][j + 1 < CPT ? j + 1 : j], -bx) * x[r][j + 1 < CPT ? j + 1 : j];
+                                else rr -= qs[r * W + c0 + CPT + 1];
+                                if (j > 0) rr -= fma(-ax, u[r][j > 0 ? j - 1 : 0], -bx) * x[r][j > 0 ? j - 1 : 0];
+                                else rr -= qs[r * W + c0];
+                                const double uNv = r + 1 < H ? u[r + 1 < H ? r + 1 : r][j] : hN[j];
+                                const double uSv = r > 0 ? u[r > 0 ? r - 1 : 0][j] : hS[j];
+                                rr -= fma(ay, uNv, -by) * xN + fma(-ay, uSv, -by) * xS + aC1 * xo;
+                            } else {
+                                const double* cf = co[LAW == 0 ? r : 0][LAW == 0 ? j : 0];
+                                const double xE = j + 1 < CPT ? x[r][j + 1 < CPT ? j + 1 : j] : qs[r * W + c0 + CPT + 1];
+                                const double xW = j > 0 ? x[r][j > 0 ? j - 1 : 0] : qs[r * W + c0];
+                                rr -= cf[1] * xE + cf[2] * xW + cf[3] * xN + cf[4] * xS + xo / cf[0];
+                            }
+                            rs2 = fma(rr, rr, rs2);
+                            rsm = fmax(rsm, fabs(rr));
                         }
-                        rs2 = fma(rr, rr, rs2);
-                        rsm = fmax(rsm, fabs(rr));
-                        bb2 = fma(b0, b0, fma(b1, b1, bb2));
+                        #pragma unroll
+                        for (int j = 0; j < CPT; ++j) bb2 = fma(bsm(r, j), bsm(r, j), bb2);
                     }
                     ac(4) += rs2;
                     ac(5) = fmax(ac(5), rsm);
@@ -551,9 +575,9 @@ struct NbEngine {
             if (st != 2) {
                 const double* Uf = S.U + (size_t)(kf % B) * nt * ns;
                 if (S.u_out)
-                    for (int i = threadIdx.x; i < nt * H * T; i += NT) {
-                        const int n = i / (H * T), rr = (i / T) % H, tt = i % T;
-                        const size_t o = (size_t)n * ns + (size_t)(r0 + rr) * NXU + 2 * tt;
+                    for (int i = threadIdx.x; i < nt * H * (NXU / 2); i += NT) {
+                        const int n = i / (H * (NXU / 2)), rr = (i / (NXU / 2)) % H, cc2 = i % (NXU / 2);
+                        const size_t o = (size_t)n * ns + (size_t)(r0 + rr) * NXU + 2 * cc2;
                         *reinterpret_cast<double2*>(S.u_out + o) = ldcg2(Uf + o);
                     }
                 if (trace && t == 0) {
@@ -575,10 +599,10 @@ struct NbEngine {
 };
 
 // Strip height h in {HB, HB + 1} and the parity of the first own row select the compile-time body.
-template <int HB, int LAW, int NXU, int DM>
-__global__ void __launch_bounds__(DM * (NXU / 2), 1) k_newton_nb(const NbParams S) {
+template <int HB, int LAW, int NXU, int DM, int CPT>
+__global__ void __launch_bounds__(DM * (NXU / CPT), 1) k_newton_nb(const NbParams S) {
     extern __shared__ double sm[];
-    using E = NbEngine<HB, LAW, NXU, DM>;
+    using E = NbEngine<HB, LAW, NXU, DM, CPT>;
     const int G = S.G, c = blockIdx.x;
     const int hb = S.P.nyu / G, hr = S.P.nyu % G;
     const int h = hb + (c < hr ? 1 : 0);
