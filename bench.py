@@ -211,7 +211,7 @@ def sync_floor(st, nit, t_newton):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None, help="GPUs (default: WORLD_SIZE, else 1)")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, help="BASELINE config 1..5 (default c5, the largest)")
@@ -223,9 +223,9 @@ def main():
     ap.add_argument("--no-guess-run", action="store_true", help="skip the coarse-guess time-to-solution run")
     args = ap.parse_args()
     ws_env = os.environ.get("WORLD_SIZE")
-    if ws_env is None and args.gpus > 1:
+    if ws_env is None and (args.gpus or 1) > 1:
         return relaunch_under_torchrun(args.gpus)
-    if ws_env is not None and int(ws_env) != args.gpus:
+    if ws_env is not None and args.gpus is not None and int(ws_env) != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}", file=sys.stderr)
         return 2
     if args.impl == "reference":

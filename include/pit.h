@@ -65,6 +65,9 @@ enum { PIT_DIRICHLET = 0, PIT_PERIODIC = 1 };           /* Eq. (2)
  * (default fast path), the Theorem 1 product form with nested level solves inside the Section 7 gate (b2), or
  * the paper's explicit form — banded P^n by Eq. (10), diag(P^n) scaling, banded LU without
  * pivoting; Dirichlet only, no gate; window = 0 means the whole horizon (N3) */
+/* AUTO = the level recurrence (asynchronous on the stream for every engine); the product forms are chosen
+ * explicitly (their window gate and Newton loop are driven from the host: one stream synchronization per Newton
+ * iteration and per gate check — DESIGN.md R19). */
 enum { PIT_INV_AUTO = 0, PIT_INV_RECURRENCE = 1, PIT_INV_PRODUCT_WINDOW = 2, PIT_INV_EXPLICIT = 3 };
 
 typedef struct {
@@ -83,7 +86,7 @@ typedef struct {
                               the Newton iteration counts of BASELINE c1-c5 are those of exact solves, DESIGN R10) */
     double  lin_atol;      /* ... or RMS(b~ - A~ x) = ||.||_2 / sqrt(ns) <= lin_atol; 0 = default 1e-4 * newton_tol */
     int32_t lin_max;       /* per-level BiCGSTAB iteration cap; 0 = default 1000 */
-    int32_t inverse_mode;  /* PIT_INV_*; AUTO = recurrence unless the product window admits all levels */
+    int32_t inverse_mode;  /* PIT_INV_*; AUTO = the level recurrence */
     int32_t window;        /* product-form window length; 0 = auto from the Section 7 gate (PRODUCT_WINDOW) or
                               the whole horizon (EXPLICIT) */
     int32_t pipeline_depth;/* Newton iterations in flight in the level wavefront; 0 = auto */
@@ -124,6 +127,20 @@ void pit_config_init(pit_config* cfg);
 /* Validate cfg, select the device, allocate all device memory.  *out = NULL on failure.
  * Errors: PIT_EINVAL (cfg NULL/invalid), PIT_ECUDA (no sm_100 device), PIT_ENOMEM. */
 int pit_create(const pit_config* cfg, pit_handle** out);
+
+/* Device bytes a handle for cfg holds (every buffer pit_create would cudaMalloc: iterate buffers, solver state,
+ * exchange cells, histories, the coarse-grid guess's nested handle), so that the caller (e.g. torch) can own the
+ * memory.  Selects the device and the engines like pit_create (needs a usable sm_100 device); allocates nothing.
+ * Errors: as pit_create (PIT_EINVAL, PIT_ECUDA).  Follows SPEC.md's run_paradin(grid, model, cfg) interface
+ * (SPEC.md:351-359): the problem statement in, the memory plan out. */
+int pit_workspace_bytes(const pit_config* cfg, size_t* bytes);
+
+/* pit_create with every create-time buffer carved from dev_ws (device memory the caller owns and keeps alive
+ * until pit_destroy; any alignment; at least pit_workspace_bytes(cfg) bytes).  pit_destroy frees nothing inside it.
+ * The product forms' scratch (pit_product_window_device, pit_explicit_window_device, inverse_mode PRODUCT_WINDOW /
+ * EXPLICIT) is grown on first use with cudaMalloc, outside the workspace.
+ * Errors: PIT_EINVAL (NULL / empty workspace), PIT_ENOMEM (workspace too small), others as pit_create. */
+int pit_create_with_workspace(const pit_config* cfg, void* dev_ws, size_t bytes, pit_handle** out);
 
 /* NULL-safe.  Frees everything pit_create allocated. */
 void pit_destroy(pit_handle* h);

@@ -81,8 +81,22 @@ struct pit_handle {
     double* nb_ctl = nullptr;     // [4] omega, sweeps, q
     double* nb_linres = nullptr;  // [MAXK][2]
     int last_engine = 0;          // engine of the last Newton solve
+    // caller-owned workspace (pit_create_with_workspace): every create-time buffer is carved from it
+    char* ws = nullptr;
+    size_t ws_size = 0, ws_off = 0;
+    bool measure = false;         // pit_workspace_bytes: size the buffers, allocate nothing
     char err[512] = {0};
 };
+
+static constexpr size_t WS_ALIGN = 256;
+static size_t ws_align(size_t b) { return (b + WS_ALIGN - 1) / WS_ALIGN * WS_ALIGN; }
+
+// Frees a buffer unless it lives in the caller's workspace.
+static void dfree(pit_handle* h, void* p) {
+    if (!p) return;
+    if (h->ws && (char*)p >= h->ws && (char*)p < h->ws + h->ws_size) return;
+    cudaFree(p);
+}
 
 static int set_err(pit_handle* h, int code, const char* fmt, ...) {
     if (h) {
@@ -167,19 +181,19 @@ static int validate(const pit_config* c, char* why, size_t n) {
 
 static void free_all(pit_handle* h) {
     for (auto& e : h->ev) if (e) { cudaEventDestroy(e); e = nullptr; }
-    cudaFree(h->U); cudaFree(h->slots); cudaFree(h->part); cudaFree(h->hpart); cudaFree(h->halo); cudaFree(h->bar);
-    cudaFree(h->hist); cudaFree(h->info); cudaFree(h->stats); cudaFree(h->d_u0); cudaFree(h->d_bc);
-    cudaFree(h->d_small); cudaFree(h->bs); cudaFree(h->trace);
-    cudaFree(h->pf_Y); cudaFree(h->pf_R); cudaFree(h->pf_dU); cudaFree(h->pf_part);
-    cudaFree(h->ex_B); cudaFree(h->ex_C5); cudaFree(h->ex_err);
-    cudaFree(h->nb_llx); cudaFree(h->nb_llu); cudaFree(h->nb_hpart); cudaFree(h->nb_sync); cudaFree(h->nb_qbits);
-    cudaFree(h->nb_ctl); cudaFree(h->nb_linres);
+    dfree(h, h->U); dfree(h, h->slots); dfree(h, h->part); dfree(h, h->hpart); dfree(h, h->halo); dfree(h, h->bar);
+    dfree(h, h->hist); dfree(h, h->info); dfree(h, h->stats); dfree(h, h->d_u0); dfree(h, h->d_bc);
+    dfree(h, h->d_small); dfree(h, h->bs); dfree(h, h->trace);
+    dfree(h, h->pf_Y); dfree(h, h->pf_R); dfree(h, h->pf_dU); dfree(h, h->pf_part);
+    dfree(h, h->ex_B); dfree(h, h->ex_C5); dfree(h, h->ex_err);
+    dfree(h, h->nb_llx); dfree(h, h->nb_llu); dfree(h, h->nb_hpart); dfree(h, h->nb_sync); dfree(h, h->nb_qbits);
+    dfree(h, h->nb_ctl); dfree(h, h->nb_linres);
     h->nb_llx = h->nb_llu = nullptr; h->nb_hpart = h->nb_ctl = h->nb_linres = nullptr; h->nb_sync = nullptr;
     h->nb_qbits = nullptr;
     h->ex_B = h->ex_C5 = nullptr; h->ex_err = nullptr; h->ex_capB = h->ex_capC = 0;
     if (h->c_march) cudaGraphExecDestroy(h->c_march);
     h->c_march = nullptr;
-    cudaFree(h->c_u0); cudaFree(h->c_ring); cudaFree(h->c_U); cudaFree(h->c_fac); cudaFree(h->c_info);
+    dfree(h, h->c_u0); dfree(h, h->c_ring); dfree(h, h->c_U); dfree(h, h->c_fac); dfree(h, h->c_info);
     h->c_u0 = h->c_ring = h->c_U = h->c_fac = nullptr; h->c_info = nullptr;
     if (h->coarse) { pit_destroy(h->coarse); h->coarse = nullptr; }
     h->bs = nullptr; h->trace = nullptr; h->pf_Y = h->pf_R = h->pf_dU = h->pf_part = nullptr;
@@ -188,9 +202,26 @@ static void free_all(pit_handle* h) {
     h->bar = nullptr; h->info = nullptr; h->stats = nullptr;
 }
 
+// Device buffer of `count` elements: carved from the caller's workspace (pit_create_with_workspace), only sized
+// (pit_workspace_bytes), or cudaMalloc'd.  `lazy` buffers (the product forms' scratch, grown on first use) always
+// come from cudaMalloc: they are outside the create-time workspace contract (pit.h).
 template <class T>
-static int dalloc(pit_handle* h, T** p, size_t count) {
+static int dalloc(pit_handle* h, T** p, size_t count, bool lazy = false) {
     const size_t b = std::max<size_t>(count, 1) * sizeof(T);
+    if (!lazy && h->measure) {
+        *p = nullptr;
+        h->bytes += (long long)ws_align(b);
+        return PIT_OK;
+    }
+    if (!lazy && h->ws) {
+        const size_t off = ws_align(h->ws_off);
+        if (off + b > h->ws_size)
+            return set_err(h, PIT_ENOMEM, "workspace of %zu bytes too small (pit_workspace_bytes)", h->ws_size);
+        *p = reinterpret_cast<T*>(h->ws + off);
+        h->ws_off = off + b;
+        h->bytes += (long long)b;
+        return PIT_OK;
+    }
     cudaError_t e = cudaMalloc((void**)p, b);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -238,6 +269,8 @@ static const void* onchip_fn(int ppt, bool trace, int law) {
     return trace ? onchip_fn_t<true, 0>(ppt) : onchip_fn_t<false, 0>(ppt);
 }
 
+static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool measure, pit_handle** out);
+
 // The c_f-coarsened problem of the initial guess: N_x / c_f, N_y / c_f intervals, N_t / c_f levels
 // of step c_f dt, same law, domain and solver settings.  "Solving Eq. (FDS) sequentially": the nested handle is
 // a ONE-level problem; build_guess marches it level by level (u^0 of level m = the converged level m-1), so its
@@ -249,8 +282,23 @@ static int create_coarse(pit_handle* h) {
     cc.nx = c.nx / f; cc.ny = c.ny / f; cc.nt = 1; cc.dt = c.dt * f;
     cc.guess_cf = 0; cc.pipeline_depth = 0; cc.engine = 0; cc.window = 0; cc.stop_norm = 0;
     cc.inverse_mode = PIT_INV_RECURRENCE;
-    int rc = pit_create(&cc, &h->coarse);
-    if (rc != PIT_OK) return set_err(h, rc, "coarse-grid handle: %s", pit_strerror(rc));
+    int rc;
+    if (h->measure) {                       // the nested handle's buffers count into this handle's workspace
+        pit_handle* m = nullptr;
+        if ((rc = create_impl(&cc, nullptr, 0, true, &m)) != PIT_OK) return set_err(h, rc, "coarse-grid handle: %s", pit_strerror(rc));
+        h->bytes += m->bytes + (long long)WS_ALIGN;
+        h->coarse = m;                      // kept for its problem constants below; freed with h (it owns nothing)
+    } else if (h->ws) {                     // nested handle carved from this handle's workspace
+        size_t need = 0;
+        if ((rc = pit_workspace_bytes(&cc, &need)) != PIT_OK) return set_err(h, rc, "coarse-grid handle: %s", pit_strerror(rc));
+        const size_t off = ws_align(h->ws_off);
+        if (off + need > h->ws_size) return set_err(h, PIT_ENOMEM, "workspace of %zu bytes too small", h->ws_size);
+        if ((rc = create_impl(&cc, h->ws + off, need, false, &h->coarse)) != PIT_OK)
+            return set_err(h, rc, "coarse-grid handle: %s", pit_strerror(rc));
+        h->ws_off = off + need;
+    } else if ((rc = pit_create(&cc, &h->coarse)) != PIT_OK) {
+        return set_err(h, rc, "coarse-grid handle: %s", pit_strerror(rc));
+    }
     GuessParams& g = h->gp;
     std::memset(&g, 0, sizeof(g));
     const Prob& P = h->P;
@@ -268,7 +316,7 @@ static int create_coarse(pit_handle* h) {
     return PIT_OK;
 }
 
-int pit_create(const pit_config* cfg, pit_handle** out) {
+static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool measure, pit_handle** out) {
     if (!out) return PIT_EINVAL;
     *out = nullptr;
     char why[256];
@@ -276,6 +324,9 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     if (rc != PIT_OK) return rc;
     pit_handle* h = new (std::nothrow) pit_handle();
     if (!h) return PIT_ENOMEM;
+    h->ws = ws;
+    h->ws_size = ws_size;
+    h->measure = measure;
     h->cfg = *cfg;
     pit_config& c = h->cfg;
     if (c.lin_rtol == 0.0) c.lin_rtol = 1e-6;     // inexact-Newton forcing term (R10)
@@ -439,8 +490,8 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     h->nb_llu_bytes = (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2 * sizeof(unsigned long long);
     bool ev_ok = true;
     for (auto& e : h->ev) ev_ok = ev_ok && cudaEventCreate(&e) == cudaSuccess;
-    if (!ev_ok || cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess ||
-        cudaMemset(h->stats, 0, (8 + MAXK) * sizeof(long long)) != cudaSuccess) {
+    if (!ev_ok || (!measure && (cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess ||
+                                cudaMemset(h->stats, 0, (8 + MAXK) * sizeof(long long)) != cudaSuccess))) {
         cudaGetLastError();
         free_all(h);
         delete h;
@@ -453,6 +504,29 @@ int pit_create(const pit_config* cfg, pit_handle** out) {
     }
     *out = h;
     return PIT_OK;
+}
+
+int pit_create(const pit_config* cfg, pit_handle** out) { return create_impl(cfg, nullptr, 0, false, out); }
+
+int pit_workspace_bytes(const pit_config* cfg, size_t* bytes) {
+    if (!bytes) return PIT_EINVAL;
+    *bytes = 0;
+    pit_handle* h = nullptr;
+    const int rc = create_impl(cfg, nullptr, 0, true, &h);
+    if (rc != PIT_OK) return rc;
+    *bytes = (size_t)h->bytes + WS_ALIGN;
+    pit_destroy(h);
+    return PIT_OK;
+}
+
+int pit_create_with_workspace(const pit_config* cfg, void* dev_ws, size_t bytes, pit_handle** out) {
+    if (!out) return PIT_EINVAL;
+    *out = nullptr;
+    if (!dev_ws || bytes == 0) return PIT_EINVAL;
+    char* base = (char*)dev_ws;
+    const size_t skew = (WS_ALIGN - (uintptr_t)base % WS_ALIGN) % WS_ALIGN;   // align the arena start
+    if (skew >= bytes) return PIT_EINVAL;
+    return create_impl(cfg, base + skew, bytes - skew, false, out);
 }
 
 void pit_destroy(pit_handle* h) {
@@ -936,8 +1010,8 @@ static int ensure_pf_scratch(pit_handle* h) {
     if (h->pf_Y) return PIT_OK;
     const long long ns = h->P.ns, N = ns * h->P.nt;
     int rc;
-    if ((rc = dalloc(h, &h->pf_Y, (size_t)(2 * N))) || (rc = dalloc(h, &h->pf_R, (size_t)N)) ||
-        (rc = dalloc(h, &h->pf_dU, (size_t)N)) || (rc = dalloc(h, &h->pf_part, (size_t)(4096 + 8))))
+    if ((rc = dalloc(h, &h->pf_Y, (size_t)(2 * N), true)) || (rc = dalloc(h, &h->pf_R, (size_t)N, true)) ||
+        (rc = dalloc(h, &h->pf_dU, (size_t)N, true)) || (rc = dalloc(h, &h->pf_part, (size_t)(4096 + 8), true)))
         return rc;
     return PIT_OK;
 }
@@ -1122,13 +1196,13 @@ static int explicit_window(pit_handle* h, int s0, int L, const double* d_U, cons
     int rc = ensure_pf_scratch(h);
     if (rc != PIT_OK) return rc;
     if (needB > h->ex_capB) {
-        cudaFree(h->ex_B); h->ex_B = nullptr; h->ex_capB = 0;
-        if ((rc = dalloc(h, &h->ex_B, (size_t)needB))) return rc;
+        dfree(h, h->ex_B); h->ex_B = nullptr; h->ex_capB = 0;
+        if ((rc = dalloc(h, &h->ex_B, (size_t)needB, true))) return rc;
         h->ex_capB = needB;
     }
     if (needC > h->ex_capC) {
-        cudaFree(h->ex_C5); h->ex_C5 = nullptr; h->ex_capC = 0;
-        if ((rc = dalloc(h, &h->ex_C5, (size_t)needC))) return rc;
+        dfree(h, h->ex_C5); h->ex_C5 = nullptr; h->ex_capC = 0;
+        if ((rc = dalloc(h, &h->ex_C5, (size_t)needC, true))) return rc;
         h->ex_capC = needC;
     }
     if (!h->ex_err) CUDA_TRY(h, cudaMalloc((void**)&h->ex_err, sizeof(unsigned)));

@@ -23,7 +23,7 @@ PIT_DIRICHLET, PIT_PERIODIC = 0, 1
 PIT_INV_AUTO, PIT_INV_RECURRENCE, PIT_INV_PRODUCT_WINDOW, PIT_INV_EXPLICIT = 0, 1, 2, 3
 
 # every symbol include/pit.h declares (tests check the library exports all of them)
-EXPORTS = ["pit_config_init", "pit_create", "pit_destroy", "pit_solve", "pit_solve_device", "pit_residual_device",
+EXPORTS = ["pit_config_init", "pit_create", "pit_workspace_bytes", "pit_create_with_workspace", "pit_destroy", "pit_solve", "pit_solve_device", "pit_residual_device",
            "pit_level_solve_device", "pit_product_window_device", "pit_explicit_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_engine_info", "pit_strerror",
            "pit_last_error", "pit_abi_version"]
 
@@ -59,6 +59,10 @@ def lib():
         L.pit_config_init.argtypes = [C.POINTER(PitConfig)]; L.pit_config_init.restype = None
         L.pit_create.argtypes = [C.POINTER(PitConfig), C.POINTER(C.c_void_p)]; L.pit_create.restype = C.c_int
         L.pit_destroy.argtypes = [hp]; L.pit_destroy.restype = None
+        L.pit_workspace_bytes.argtypes = [C.POINTER(PitConfig), C.POINTER(C.c_size_t)]
+        L.pit_workspace_bytes.restype = C.c_int
+        L.pit_create_with_workspace.argtypes = [C.POINTER(PitConfig), vp, C.c_size_t, C.POINTER(C.c_void_p)]
+        L.pit_create_with_workspace.restype = C.c_int
         L.pit_solve.argtypes = [hp, dp, dp, dp, dp, dp, i32p]; L.pit_solve.restype = C.c_int
         L.pit_solve_device.argtypes = [hp, dp, dp, dp, dp, dp, i32p, vp]; L.pit_solve_device.restype = C.c_int
         L.pit_residual_device.argtypes = [hp, dp, dp, dp, dp, dp, dp, vp]; L.pit_residual_device.restype = C.c_int
@@ -107,14 +111,31 @@ def _stream(stream) -> Optional[int]:
     return getattr(stream, "cuda_stream", stream)
 
 
-class Solver:
-    """One libpit handle for one problem shape (pit_create / pit_destroy)."""
+def workspace_bytes(p: W.Problem, **cfg_over) -> int:
+    """pit_workspace_bytes: the device bytes a handle for problem ``p`` holds."""
+    cfg = make_config(p, **cfg_over)
+    n = C.c_size_t(0)
+    rc = lib().pit_workspace_bytes(C.byref(cfg), C.byref(n))
+    if rc != 0:
+        raise PitError(rc, lib().pit_strerror(rc).decode())
+    return int(n.value)
 
-    def __init__(self, p: W.Problem, **cfg_over):
+
+class Solver:
+    """One libpit handle for one problem shape (pit_create / pit_destroy).  ``workspace``: a device buffer (a torch
+    tensor of >= workspace_bytes(p) bytes) the handle carves its memory from (pit_create_with_workspace); the
+    Solver keeps a reference to it."""
+
+    def __init__(self, p: W.Problem, workspace=None, **cfg_over):
         self.problem = p
         self.cfg = make_config(p, **cfg_over)
+        self.workspace = workspace
         h = C.c_void_p()
-        rc = lib().pit_create(C.byref(self.cfg), C.byref(h))
+        if workspace is None:
+            rc = lib().pit_create(C.byref(self.cfg), C.byref(h))
+        else:
+            nbytes = workspace.numel() * workspace.element_size()
+            rc = lib().pit_create_with_workspace(C.byref(self.cfg), C.c_void_p(workspace.data_ptr()), nbytes, C.byref(h))
         if rc != 0:
             raise PitError(rc, lib().pit_strerror(rc).decode())
         self.h = h

@@ -280,3 +280,64 @@ def test_merged_first_iteration(c, nt, monkeypatch):
         assert s0["grid_barriers"] - s1["grid_barriers"] == s1["steps"]
     seq = O.solve_sequential(p, levels=min(nt, 2))
     assert normwise_rel(U1[:seq.U.shape[0]], seq.U) <= 1e-10
+
+
+@pytest.mark.parametrize("name,make,cfg", [
+    ("c5_prefix_engine4", lambda: W.config(5, nt=6), {}),
+    ("c3_prefix_engine3", lambda: W.config(3, nt=3), {"engine": 3}),
+    ("paper_heat_coarse_guess", lambda: W.paper_heat(16), {"guess_cf": 4}),
+])
+def test_solve_inside_a_caller_owned_workspace(name, make, cfg):
+    """pit_workspace_bytes / pit_create_with_workspace: a handle whose every create-time buffer lives
+    in a torch-allocated workspace (deliberately misaligned by 8 bytes) gives bit-identical results to a
+    cudaMalloc'd handle, and allocates no device memory of its own."""
+    from gpu_util import torch_cuda
+    torch = torch_cuda()
+    p = make()
+    need = pit.workspace_bytes(p, **cfg)
+    ref = gpu_solve(p, **cfg)
+    ws = torch.empty(need + 8, dtype=torch.uint8, device="cuda")[8:]
+    free0 = torch.cuda.mem_get_info()[0]
+    s = pit.Solver(p, workspace=ws, **cfg)
+    try:
+        assert torch.cuda.mem_get_info()[0] >= free0 - (2 << 20)   # nothing beyond driver-level noise
+        d_u0 = torch.from_numpy(p.u0).cuda()
+        d_ring = None if p.ring is None else torch.from_numpy(p.ring).cuda()
+        d_out = torch.empty((p.nt, p.ns), dtype=torch.float64, device="cuda")
+        d_hist = torch.zeros((s.cfg.newton_max, 4), dtype=torch.float64, device="cuda")
+        d_info = torch.zeros(2, dtype=torch.int32, device="cuda")
+        s.solve_device(d_u0, d_ring, None, d_out, d_hist, d_info)
+        torch.cuda.synchronize()
+        nit, st = (int(v) for v in d_info.cpu())
+        assert (nit, st) == (ref[2], ref[3])
+        assert np.array_equal(d_out.cpu().numpy(), ref[0])
+    finally:
+        s.close()
+    # too small a workspace is refused
+    small = torch.empty(need // 2, dtype=torch.uint8, device="cuda")
+    with pytest.raises(pit.PitError):
+        pit.Solver(p, workspace=small, **cfg)
+
+
+def test_solve_device_is_asynchronous_for_every_default_path():
+    """pit_solve_device returns before the solve finishes (no host synchronization on the default AUTO path: the
+    level recurrence on every engine), with a long kernel queued ahead on the same stream."""
+    from gpu_util import torch_cuda
+    torch = torch_cuda()
+    for p in (W.config(1), W.config(2)):
+        s = pit.Solver(p)
+        try:
+            st = torch.cuda.Stream()
+            d_u0 = torch.from_numpy(p.u0).cuda()
+            d_out = torch.empty((p.nt, p.ns), dtype=torch.float64, device="cuda")
+            d_hist = torch.zeros((s.cfg.newton_max, 4), dtype=torch.float64, device="cuda")
+            d_info = torch.zeros(2, dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                torch.cuda._sleep(200_000_000)          # ~0.1 s of GPU time ahead of the solve
+                s.solve_device(d_u0, None, None, d_out, d_hist, d_info, stream=st)
+                assert not st.query(), "pit_solve_device waited for the stream"
+            st.synchronize()
+            assert int(d_info[1].item()) in (0, 1)
+        finally:
+            s.close()
