@@ -199,6 +199,19 @@ int pit_explicit_window_device(pit_handle* h, int32_t s0, int32_t L, const doubl
                                const double* d_bc, const double* d_R, const double* d_carry, double* d_dU,
                                int32_t* d_info, void* cuda_stream);
 
+/* N4 — one step of the multi-GPU time-slab pipeline: ONE all-at-once Newton iteration (Eq. (5)-(7),
+ * PAPER.md:86-156) over this handle's nt levels taken as levels s..s+nt-1 of a longer horizon.  The recursion of
+ * Eq. (7) continues across the slab boundary: level s's residual uses d_uprev = U_k at level s-1 (u^0 for the first
+ * slab) and its solve starts from  b = r^s + d_carry_in  (d_carry_in = du_k of level s-1, NULL = 0 for the first
+ * slab).  Inputs d_U_k [nt][ns] (iterate k of the slab), d_bc the slab's Dirichlet rings; outputs d_U_k1 [nt][ns] =
+ * U_k + dU, d_carry_out [ns] = du_k of the slab's last level (the next slab's carry; may be NULL), d_hist [4] = the
+ * slab's { rms R(U_k), max|R(U_k)|, rms dU_k, max|dU_k| } over its nt ns unknowns (combine slabs by sums of
+ * squares and maxima; the stop rule is the caller's), d_info [2] (may be NULL).  Engine 4 only (PIT_EINVAL
+ * otherwise); all pointers device, 16-byte aligned; asynchronous on cuda_stream. */
+int pit_slab_iterate_device(pit_handle* h, const double* d_uprev, const double* d_carry_in, const double* d_bc,
+                            const double* d_U_k, double* d_U_k1, double* d_carry_out, double* d_hist, int32_t* d_info,
+                            void* cuda_stream);
+
 /* The initial Newton iterate on its own: with guess_cf >= 2 the coarse-grid solve + spline
  * interpolation described at pit_config.guess_cf, else u^0 at every level; written to d_U0 [nt][ns] (device).
  * d_u0 [ns], d_bc as in pit_solve_device.  Asynchronous on cuda_stream. */

@@ -57,6 +57,8 @@ def lib():
         L.or_solve_allatonce.argtypes = [P, dp, C.c_void_p, C.c_void_p, C.c_double, C.c_int, dp, dp,
                                          C.POINTER(C.c_int)]
         L.or_solve_allatonce.restype = C.c_int
+        L.or_allatonce_iteration.argtypes = [P, dp, C.c_void_p, C.c_void_p, dp, dp, C.c_void_p, dp]
+        L.or_allatonce_iteration.restype = C.c_int
         L.or_spacetime_residual.argtypes = [P, dp, C.c_void_p, dp, dp]
         L.or_spacetime_residual.restype = None
         _lib = L
@@ -193,3 +195,20 @@ def spacetime_residual(p, U) -> np.ndarray:
     ring = None if (p.bc != 0 or p.ring is None) else _f64(p.ring)
     lib().or_spacetime_residual(C.byref(pr), _f64(p.u0), _ptr(ring), _f64(np.asarray(U).reshape(-1)), R)
     return R.reshape(p.nt, ns)
+
+
+def allatonce_iteration(p, u_prev, carry_in, Uk):
+    """ONE all-at-once Newton iteration over a slab (levels 1..p.nt after the level u_prev, incoming carry
+    carry_in or None = 0): returns (U_{k+1}, carry_out, sums {sum R^2, max|R|, sum dU^2, max|dU|})."""
+    pr = _prob(p)
+    ns = lib().or_ns(C.byref(pr))
+    Uk1 = np.empty(p.nt * ns)
+    cout = np.empty(ns)
+    sums = np.zeros(4)
+    ring = None if (p.bc != 0 or p.ring is None) else _f64(p.ring)
+    ci = None if carry_in is None else _f64(carry_in)
+    rc = lib().or_allatonce_iteration(C.byref(pr), _f64(u_prev), _ptr(ci), _ptr(ring), _f64(np.asarray(Uk).reshape(-1)),
+                                      Uk1, cout.ctypes.data_as(C.c_void_p), sums)
+    if rc != 0:
+        raise RuntimeError(f"or_allatonce_iteration rc={rc}")
+    return Uk1.reshape(p.nt, ns), cout, sums

@@ -422,6 +422,51 @@ int or_solve_allatonce(const or_prob* p, const double* u0, const double* bc, con
     return status;
 }
 
+/*
+ * Test-only: ONE all-at-once Newton iteration (Eq. (5)-(7)) over a SLAB of levels 1..nt (p->nt)
+ * whose preceding level is u_prev (U_k at the level before the slab; u^0 for the first slab) and whose incoming
+ * carry is carry_in (Delta u_k at that level; NULL = 0 for the first slab).  The forward recursion of Eq. (7) then
+ * starts from carry_in instead of 0,  Delta u^1 = A_1^{-1} (r^1 + carry_in)  — the exact continuation of the
+ * recursion across a slab boundary, which is what the multi-GPU time-slab pipeline runs.
+ * Outputs U_{k+1} = U_k + Delta U (Uk1), carry_out = Delta u^{nt} (may be NULL) and
+ * sums[4] = { sum R(U_k)^2, max|R(U_k)|, sum dU^2, max|dU| } over the slab.
+ */
+int or_allatonce_iteration(const or_prob* p, const double* u_prev, const double* carry_in, const double* bc,
+                           const double* Uk, double* Uk1, double* carry_out, double* sums) {
+    const long n = or_ns(p);
+    const int rl = or_ring_len(p);
+    double* w = (double*)malloc(sizeof(double) * (size_t)(8 * n));
+    if (!w) return OR_ENOMEM;
+    double *aC = w, *aE = w + n, *aW = w + 2 * n, *aN = w + 3 * n, *aS = w + 4 * n, *b = w + 5 * n, *dl = w + 6 * n;
+    double* Rl = w + 7 * n;
+    double rs = 0.0, rm = 0.0, ds = 0.0, dm = 0.0;
+    if (carry_in) memcpy(dl, carry_in, sizeof(double) * (size_t)n);
+    else memset(dl, 0, sizeof(double) * (size_t)n);
+    for (int lv = 1; lv <= p->nt; ++lv) {
+        const double* ring = (p->bc == 0 && bc) ? bc + (long)(lv - 1) * rl : NULL;
+        const double* ul = Uk + (long)(lv - 1) * n;
+        or_residual(p, ul, lv == 1 ? u_prev : Uk + (long)(lv - 2) * n, ring, Rl);
+        or_jacobian(p, ul, ring, aC, aE, aW, aN, aS);
+        for (long q = 0; q < n; ++q) {
+            Rl[q] = -Rl[q];
+            rs += Rl[q] * Rl[q];
+            if (fabs(Rl[q]) > rm) rm = fabs(Rl[q]);
+            b[q] = Rl[q] + dl[q];                                          /* r^n + Delta u^{n-1} */
+        }
+        int rc = or_linear_solve(p, aC, aE, aW, aN, aS, b, dl);
+        if (rc < 0) { free(w); return rc; }
+        for (long q = 0; q < n; ++q) {
+            Uk1[(long)(lv - 1) * n + q] = ul[q] + dl[q];
+            ds += dl[q] * dl[q];
+            if (fabs(dl[q]) > dm) dm = fabs(dl[q]);
+        }
+    }
+    if (carry_out) memcpy(carry_out, dl, sizeof(double) * (size_t)n);
+    sums[0] = rs; sums[1] = rm; sums[2] = ds; sums[3] = dm;
+    free(w);
+    return OR_OK;
+}
+
 /* Space-time residual of a given U (all levels): R = -G^n(U^n; U^{n-1}), used by the full-size
  * parity tests to check a GPU solution against the discrete equations of Eq. (4). */
 void or_spacetime_residual(const or_prob* p, const double* u0, const double* bc, const double* U, double* R) {

@@ -71,6 +71,7 @@ struct pit_handle {
     bool nb = false;              // the Newton solve runs on engine 4
     int nb_rmax = 0, nb_G = 0, nb_D = 0, nb_dm = 0;   // base strip height, CTAs, iterations in flight, warp groups
     int nb_threads = 0;                               // threads per CTA
+    bool nb_ctl_ready = false;                        // slab iterations: omega / sweeps fixed at the first call
     size_t nb_smem = 0;
     unsigned long long* nb_llx = nullptr;   // LL cells, x publications
     unsigned long long* nb_llu = nullptr;   // LL cells, U boundary-row publications
@@ -639,25 +640,32 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
 // persistent neighbour-synchronised kernel.  The LL cells and the per-iteration counters are cleared first, so a
 // publication number never matches a cell of an earlier solve.
 static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, double* d_u_out, double* d_hist, int* d_info,
-                     cudaStream_t st) {
+                     cudaStream_t st, const double* carry_in = nullptr, double* carry_out = nullptr, bool one_iteration = false) {
     const Prob& P = h->P;
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_llx, 0, h->nb_llx_bytes, st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_llu, 0, h->nb_llu_bytes, st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_sync, 0, sizeof(unsigned) * 2 * MAXK, st));
-    CUDA_TRY(h, cudaMemsetAsync(h->nb_qbits, 0, sizeof(unsigned long long), st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_linres, 0, sizeof(double) * 2 * MAXK, st));
     CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
-    nb_setup_launch(P, h->U, ring, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
-                    std::max(1, std::min(grid_for(P.ns, h->sms), 2 * h->sms)), st);
-    CUDA_TRY(h, cudaGetLastError());
+    // omega and the sweep count from the Jacobi bound of A_1 at the initial iterate; a time slab keeps the values of
+    // its first iteration for the later ones (the relaxation then does not change between Newton iterations)
+    if (!(one_iteration && h->nb_ctl_ready)) {
+        CUDA_TRY(h, cudaMemsetAsync(h->nb_qbits, 0, sizeof(unsigned long long), st));
+        nb_setup_launch(P, h->U, ring, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
+                        std::max(1, std::min(grid_for(P.ns, h->sms), 2 * h->sms)), st);
+        CUDA_TRY(h, cudaGetLastError());
+        h->nb_ctl_ready = one_iteration;
+    }
     NbParams S;
     std::memset(&S, 0, sizeof(S));
-    S.P = P; S.u0 = d_u0; S.ring = ring; S.U = h->U; S.B = h->B; S.D = h->nb_D; S.G = h->nb_G;
+    S.P = P; S.u0 = d_u0; S.ring = ring; S.U = h->U; S.B = h->B; S.D = one_iteration ? 1 : h->nb_D; S.G = h->nb_G;
     S.ctl = h->nb_ctl; S.llx = h->nb_llx; S.llu = h->nb_llu; S.hpart = h->nb_hpart;
     S.arrive = h->nb_sync; S.decided = h->nb_sync + MAXK;
     S.hist = d_hist ? d_hist : h->hist; S.linres = h->nb_linres; S.info = d_info ? d_info : h->info;
-    S.u_out = d_u_out; S.newton_tol = h->cfg.newton_tol; S.newton_max = h->cfg.newton_max; S.stop_norm = h->cfg.stop_norm;
+    S.u_out = d_u_out; S.newton_tol = h->cfg.newton_tol; S.newton_max = one_iteration ? 1 : h->cfg.newton_max;
+    S.stop_norm = h->cfg.stop_norm;
+    S.carry_in = carry_in; S.carry_out = carry_out;
     S.stats = h->stats;
     S.trace = h->trace ? h->trace + 13 : nullptr;
     void* args[] = {(void*)&S};
@@ -894,6 +902,23 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
     S.mode = 0;
     h->last_engine = h->engine;
     return launch_newton(h, S, st);
+}
+
+// N4: one all-at-once Newton iteration over this handle's levels as a time slab of a longer horizon (engine 4).
+int pit_slab_iterate_device(pit_handle* h, const double* d_uprev, const double* d_carry_in, const double* d_bc,
+                            const double* d_U_k, double* d_U_k1, double* d_carry_out, double* d_hist, int32_t* d_info,
+                            void* cuda_stream) {
+    if (!h || !d_uprev || !d_U_k || !d_U_k1 || !d_hist) return set_err(h, PIT_EINVAL, "null argument");
+    if (!h->nb) return set_err(h, PIT_EINVAL, "time-slab iterations need engine 4 (pit_config.engine)");
+    if (((uintptr_t)d_uprev | (uintptr_t)d_U_k | (uintptr_t)d_U_k1 | (uintptr_t)d_carry_in | (uintptr_t)d_carry_out) % 16)
+        return set_err(h, PIT_EINVAL, "device buffers must be 16-byte aligned");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    h->launches = 0;
+    int rc = launch_init(h, d_uprev, d_U_k, st);
+    if (rc != PIT_OK) return rc;
+    return launch_nb(h, d_uprev, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_U_k1, d_hist, (int*)d_info, st, d_carry_in,
+                     d_carry_out, true);
 }
 
 int pit_initial_guess_device(pit_handle* h, const double* d_u0, const double* d_bc, double* d_U0, void* cuda_stream) {

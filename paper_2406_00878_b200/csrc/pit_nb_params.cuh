@@ -33,6 +33,8 @@ struct NbParams {
     int newton_max, stop_norm;
     long long* stats;           // [8 + MAXK]
     unsigned long long* trace;  // optional [G][NB_TR] cycle accounts (nullptr = off)
+    const double* carry_in;     // time slab (N4): du_k of the level before level 1 [ns] (nullptr = 0), first pass
+    double* carry_out;          // time slab (N4): du_k of level nt [ns] (nullptr = not written)
 };
 constexpr int NB_TR = 8;        // trace: prologue, sweeps, sweep waits, epilogue, iteration reductions, pass ends, total
 

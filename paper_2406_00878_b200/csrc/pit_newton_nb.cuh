@@ -201,10 +201,17 @@ struct NbEngine {
         for (int pass = 0;; ++pass) {
             const int k = pass * D + p;
             const bool active = p < D && k < S.newton_max;
+            // carry du^0: 0, or (time slab, N4) the previous slab's du_k of the level before level 1
+            const double* cin = (pass == 0 && p == 0) ? S.carry_in : nullptr;
             #pragma unroll
             for (int r = 0; r < H; ++r)
                 #pragma unroll
-                for (int j = 0; j < CPT; ++j) x[r][j] = 0.0;   // carry du^0 = 0
+                for (int j = 0; j < CPT; j += 2) {
+                    double2 v = make_double2(0.0, 0.0);
+                    if (cin) v = ldcg2(cin + (size_t)(r0 + r) * NXU + c0 + j);
+                    x[r][j] = v.x;
+                    x[r][j + 1] = v.y;
+                }
             lastx = -1;
             for (int n = 1; active && n <= nt; ++n) {
                 ++levels;
@@ -314,6 +321,13 @@ struct NbEngine {
                         double xs_h[HC], xn_h[HC];
                         #pragma unroll
                         for (int h = 0; h < HC; ++h) xs_h[h] = xn_h[h] = 0.0;
+                        if (lastx < 0 && cin) {   // first half-sweep of a slab: the carry's halo rows
+                            #pragma unroll
+                            for (int h = 0; h < HC; ++h) {
+                                if (cs >= 0) xs_h[h] = __ldcg(cin + (size_t)((r0 - 1 + nyu) % nyu) * NXU + c0 + ((PR0 + cc) & 1) + 2 * h);
+                                if (cn >= 0) xn_h[h] = __ldcg(cin + (size_t)((r0 + H) % nyu) * NXU + c0 + ((PR0 + H - 1 + cc) & 1) + 2 * h);
+                            }
+                        }
                         if (lastx >= 0) {
                             const unsigned qn = (unsigned)lastx;
                             LLc hs[HC], hn[HC];
@@ -419,6 +433,12 @@ struct NbEngine {
                     ++qu;
                     ac(2) += d2;
                     ac(3) = fmax(ac(3), dm);
+                    if (n == nt && S.carry_out && pass == 0 && p == 0)   // time slab: du_k of the last level
+                        #pragma unroll
+                        for (int r = 0; r < H; ++r)
+                            #pragma unroll
+                            for (int j = 0; j < CPT; j += 2)
+                                *reinterpret_cast<double2*>(S.carry_out + (size_t)(r0 + r) * NXU + c0 + j) = make_double2(x[r][j], x[r][j + 1]);
                     gbar();                               // every thread's U_{k+1}^n rows are written
                     if (t == 0) {
                         __threadfence_block();

@@ -24,7 +24,7 @@ PIT_INV_AUTO, PIT_INV_RECURRENCE, PIT_INV_PRODUCT_WINDOW, PIT_INV_EXPLICIT = 0, 
 
 # every symbol include/pit.h declares (tests check the library exports all of them)
 EXPORTS = ["pit_config_init", "pit_create", "pit_workspace_bytes", "pit_create_with_workspace", "pit_destroy", "pit_solve", "pit_solve_device", "pit_residual_device",
-           "pit_level_solve_device", "pit_product_window_device", "pit_explicit_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_engine_info", "pit_strerror",
+           "pit_level_solve_device", "pit_product_window_device", "pit_slab_iterate_device", "pit_explicit_window_device", "pit_initial_guess_device", "pit_sizes", "pit_stats", "pit_engine_info", "pit_strerror",
            "pit_last_error", "pit_abi_version"]
 
 
@@ -73,6 +73,8 @@ def lib():
         L.pit_explicit_window_device.argtypes = [hp, C.c_int32, C.c_int32, dp, dp, dp, dp, dp, dp, i32p, vp]
         L.pit_explicit_window_device.restype = C.c_int
         L.pit_initial_guess_device.argtypes = [hp, dp, dp, dp, vp]; L.pit_initial_guess_device.restype = C.c_int
+        L.pit_slab_iterate_device.argtypes = [hp, dp, dp, dp, dp, dp, dp, dp, i32p, vp]
+        L.pit_slab_iterate_device.restype = C.c_int
         L.pit_sizes.argtypes = [hp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]; L.pit_sizes.restype = C.c_int
         L.pit_stats.argtypes = [hp, C.POINTER(C.c_int64), C.c_int32]; L.pit_stats.restype = C.c_int
         L.pit_engine_info.argtypes = [hp, C.POINTER(C.c_double), C.c_int32]; L.pit_engine_info.restype = C.c_int
@@ -179,6 +181,12 @@ class Solver:
 
     def initial_guess_device(self, d_u0, d_ring, d_U0, stream=None) -> int:
         return self._check(lib().pit_initial_guess_device(self.h, _ptr(d_u0), _ptr(d_ring), _ptr(d_U0), _stream(stream)))
+
+    def slab_iterate_device(self, d_uprev, d_carry_in, d_ring, d_U_k, d_U_k1, d_carry_out, d_hist, d_info=None,
+                            stream=None) -> int:
+        return self._check(lib().pit_slab_iterate_device(self.h, _ptr(d_uprev), _ptr(d_carry_in), _ptr(d_ring),
+                                                         _ptr(d_U_k), _ptr(d_U_k1), _ptr(d_carry_out), _ptr(d_hist),
+                                                         _ptr(d_info), _stream(stream)))
 
     def level_solve_device(self, level, d_U, d_ring, d_b, d_x, d_info, stream=None) -> int:
         return self._check(lib().pit_level_solve_device(self.h, level, _ptr(d_U), _ptr(d_ring), _ptr(d_b),
