@@ -209,6 +209,59 @@ def sync_floor(st, nit, t_newton):
             "source": "tools/barrier_bench.cu (profiles/r01d/barrier_bench.txt)"}
 
 
+def run_timeslab(args):
+    """N4: ONE solve of the config with its levels split into slabs over the ranks (paper_2406_00878_b200/timeslab.py):
+    strong scaling.  Device time = max over ranks of the solve's span (CUDA events around each rank's pipeline)."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % _free_port(), rank=0, world_size=1)
+    from paper_2406_00878_b200 import timeslab as TS, workloads as W
+    p = W.config(args.config)
+    s, e = TS.split_levels(p.nt, ws)[rank]
+    q = TS.slab_problem(p, s, e)
+    wk = TS.GpuSlabWorker(q, device=local)
+    comm = TS.TorchComm(device=dev if ws > 1 else None)
+    u0 = torch.from_numpy(p.u0).to(dev)
+    U0 = torch.from_numpy(np.tile(p.u0, (q.nt, 1))).to(dev)
+    times = []
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = TS.solve_timeslab(wk, comm, p.nt, p.ns, u0, U0, newton_tol=p.newton_tol)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        if it >= args.warmup:
+            times.append(e0.elapsed_time(e1))
+    ms = max_over_ranks(float(np.median(times)), dev if ws > 1 else None)
+    if rank == 0:
+        line = {"metric": METRIC, "value": float(p.dof) * r.n_iter / (ms * 1e-3), "unit": UNIT, "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": p.name, "nt": p.nt, "grid": [p.nxu, p.nyu], "mode": "timeslab (N4)",
+                           "slabs": TS.split_levels(p.nt, ws), "newton_iterations": r.n_iter, "status": r.status,
+                           "iterations_run": r.iterations_run, "parallelism": f"time slabs x{ws}"}}
+        print(json.dumps(line), flush=True)
+    wk.close()
+    dist.destroy_process_group()
+    return 0
+
+
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=None, help="GPUs (default: WORLD_SIZE, else 1)")
@@ -221,6 +274,9 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=15.0, help="seconds of oracle work per reference step")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-guess-run", action="store_true", help="skip the coarse-guess time-to-solution run")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "timeslab"],
+                    help="N > 1: independent replicas (default; the configs are single-GPU problems) or the N4 time-slab "
+                         "pipeline (one solve of the config, its levels split over the ranks; strong scaling)")
     args = ap.parse_args()
     ws_env = os.environ.get("WORLD_SIZE")
     if ws_env is None and (args.gpus or 1) > 1:
@@ -230,6 +286,8 @@ def main():
         return 2
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "timeslab":
+        return run_timeslab(args)
 
     import torch
     ws, rank, local = dist_env()

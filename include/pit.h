@@ -35,6 +35,14 @@
  *           PIT_ECUDA.
  *   Determinism: identical inputs and configuration on the same GPU give bit-identical outputs
  *           (fixed-order reductions, no floating-point atomics).
+ *   Debug environment (developer instrumentation and A/B switches used for the measurements in DESIGN.md; read
+ *           once per handle at pit_create; none is needed for correct results, the defaults are the product path):
+ *             PIT_TRACE=1        cycle accounting of the persistent kernels (pit_stats, pit_engine_info)
+ *             PIT_RESJAC_V1=1    kernel (a) without TMA staging;  PIT_RESJAC_RT / PIT_RESJAC_NS  its tile rows / stages
+ *             PIT_X0=0           engines 2-3 start each level solve from 0 instead of the carry du^{n-1}
+ *             PIT_MERGE=0        engine 3 without the merged first BiCGSTAB iteration
+ *             PIT_GUESS_GRAPH=0  the coarse-grid guess's level march without a CUDA graph
+ *           All NVTX ranges ("pit_solve_device", "pit_solve", ...) are emitted unconditionally (free without a tool).
  */
 #ifndef PIT_H
 #define PIT_H

@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if failed:
             raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
         tmp = LIB + f".{tag}"
-        link = subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
+        link = subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"], capture_output=True, text=True)
         if link.returncode != 0:
             raise RuntimeError(f"link failed:\n{link.stderr}")
         os.replace(tmp, LIB)

@@ -6,6 +6,7 @@
 #include "pit.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -22,6 +23,12 @@
 #include "pit_nb_params.cuh"
 
 using namespace pit;
+
+// NVTX range around each stage the host issues (visible in nsys / ncu --nvtx; no cost without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct pit_handle {
     pit_config cfg;
@@ -82,6 +89,16 @@ struct pit_handle {
     double* nb_ctl = nullptr;     // [4] omega, sweeps, q
     double* nb_linres = nullptr;  // [MAXK][2]
     int last_engine = 0;          // engine of the last Newton solve
+    // developer switches (pit.h "Debug environment"), read once at pit_create so a handle never changes path
+    struct {
+        bool trace = false;       // PIT_TRACE: cycle accounting of the persistent kernels
+        bool resjac_v1 = false;   // PIT_RESJAC_V1: kernel (a) without TMA staging
+        int resjac_rt = 0, resjac_ns = 0;   // PIT_RESJAC_RT / _NS: kernel (a) tile rows / pipeline stages
+        int x0carry = 1;          // PIT_X0=0: engines 2-3 start level solves from 0 instead of the carry
+        bool merge = true;        // PIT_MERGE=0: engine 3 without the merged first BiCGSTAB iteration
+        bool guess_graph = true;  // PIT_GUESS_GRAPH=0: the coarse-grid march without a CUDA graph
+    } dbg;
+    int c_march_ring = -1;        // the ring presence the coarse-march graph was captured with (-1: none captured)
     // caller-owned workspace (pit_create_with_workspace): every create-time buffer is carved from it
     char* ws = nullptr;
     size_t ws_size = 0, ws_off = 0;
@@ -329,6 +346,16 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
     h->ws_size = ws_size;
     h->measure = measure;
     h->cfg = *cfg;
+    {
+        auto env_int = [](const char* n, int dflt) { const char* v = getenv(n); return v ? atoi(v) : dflt; };
+        h->dbg.trace = getenv("PIT_TRACE") != nullptr;
+        h->dbg.resjac_v1 = getenv("PIT_RESJAC_V1") != nullptr;
+        h->dbg.resjac_rt = env_int("PIT_RESJAC_RT", 0);
+        h->dbg.resjac_ns = env_int("PIT_RESJAC_NS", 0);
+        h->dbg.x0carry = env_int("PIT_X0", 1);
+        h->dbg.merge = env_int("PIT_MERGE", 1) != 0;
+        h->dbg.guess_graph = env_int("PIT_GUESS_GRAPH", 1) != 0;
+    }
     pit_config& c = h->cfg;
     if (c.lin_rtol == 0.0) c.lin_rtol = 1e-6;     // inexact-Newton forcing term (R10)
     if (c.lin_atol == 0.0) c.lin_atol = 1e-4 * c.newton_tol;
@@ -475,7 +502,7 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
         (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
         (rc = dalloc(h, &h->d_small, 2 * 1024 + 2)) ||
         (rc = dalloc(h, &h->bs, 1)) ||
-        (getenv("PIT_TRACE") && (rc = dalloc(h, &h->trace, 13 + 13 * GMAX2))) ||
+        (h->dbg.trace && (rc = dalloc(h, &h->trace, 13 + 13 * GMAX2))) ||
         (h->nb && ((rc = dalloc(h, &h->nb_llx, (size_t)h->nb_G * h->nb_dm * NB_RX * 2 * (P.nxu / 2) * 2)) ||
                    (rc = dalloc(h, &h->nb_llu, (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2)) ||
                    (rc = dalloc(h, &h->nb_hpart, (size_t)MAXK * h->nb_G * NB_NP)) ||
@@ -555,15 +582,15 @@ static int launch_resjac(pit_handle* h, int grid, cudaStream_t st, const double*
                          double* R, double* diag, double* part) {
     const Prob& P = h->P;
     const bool law1 = P.pde == PIT_BURGERS && P.m2 == 0.0;
-    const bool aligned = (P.nxu % 2 == 0) && ((uintptr_t)U % 16 == 0) && ((uintptr_t)u0 % 16 == 0) && !getenv("PIT_RESJAC_V1");
+    const bool aligned = (P.nxu % 2 == 0) && ((uintptr_t)U % 16 == 0) && ((uintptr_t)u0 % 16 == 0) && !h->dbg.resjac_v1;
     if (aligned) {
         const int rowd = P.nxu;
         // two stages filling the shared memory: the per-tile cost (halo rows, barrier round trips) amortised
         // over the largest tile (c5: 13 rows of 512, 2 x 112 KB)
         int NS = 2;
         int RT = std::max(1, std::min(P.nyu, ((224 * 1024) / (NS * rowd * 8) - 2) / 2));
-        if (getenv("PIT_RESJAC_RT")) RT = std::max(1, atoi(getenv("PIT_RESJAC_RT")));
-        if (getenv("PIT_RESJAC_NS")) NS = std::max(2, std::min(MAXSTAGE, atoi(getenv("PIT_RESJAC_NS"))));
+        if (h->dbg.resjac_rt > 0) RT = h->dbg.resjac_rt;
+        if (h->dbg.resjac_ns > 0) NS = std::max(2, std::min(MAXSTAGE, h->dbg.resjac_ns));
         const size_t smem = (size_t)NS * (2 * RT + 2) * rowd * sizeof(double);
         if (smem <= 224 * 1024) {
             const long long ntiles = (long long)P.nt * ((P.nyu + RT - 1) / RT);
@@ -605,19 +632,19 @@ static SolveParams base_params(pit_handle* h) {
 }
 
 static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
+    NvtxRange nvtx_("engines1-3 k_newton*");
     void* args[] = {(void*)&S};
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
     if (h->engine >= 2) {
         S.hmax = h->hmax;
         S.bs = h->bs;
         S.trace = h->trace;
-        S.x0carry = getenv("PIT_X0") ? atoi(getenv("PIT_X0")) : 1;   // default: start from du^{n-1}
+        S.x0carry = h->dbg.x0carry;   // default: start from du^{n-1}
         S.halo = h->halo;
         {   // merged first BiCGSTAB iteration: engine 3 Newton solves on periodic grids, strips >= 3 rows
-            const char* me_ = getenv("PIT_MERGE");
             const int Cmax = (h->G + h->D - 1) / h->D;
             S.merge = (h->engine == 3 && S.mode == 0 && h->P.bc == PIT_PERIODIC && S.x0carry &&
-                       h->P.nyu / Cmax >= 3 && !(me_ && atoi(me_) == 0)) ? 1 : 0;
+                       h->P.nyu / Cmax >= 3 && h->dbg.merge) ? 1 : 0;
         }
         if (h->trace) CUDA_TRY(h, cudaMemsetAsync(h->trace, 0, 13 * sizeof(unsigned long long), st));
         CUDA_TRY(h, cudaMemsetAsync(h->bs, 0, sizeof(BarState), st));
@@ -641,6 +668,7 @@ static int launch_newton(pit_handle* h, SolveParams& S, cudaStream_t st) {
 // publication number never matches a cell of an earlier solve.
 static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, double* d_u_out, double* d_hist, int* d_info,
                      cudaStream_t st, const double* carry_in = nullptr, double* carry_out = nullptr, bool one_iteration = false) {
+    NvtxRange nvtx_("engine4 k_newton_nb");
     const Prob& P = h->P;
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_llx, 0, h->nb_llx_bytes, st));
@@ -682,6 +710,7 @@ static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, doub
 
 // k_init_iterate bracketed by events (per-kernel device time on the launching stream, for bench.py)
 static int launch_init(pit_handle* h, const double* d_u0, const double* d_guess, cudaStream_t st) {
+    NvtxRange nvtx_("k_init_iterate");
     const long long N = h->P.ns * h->P.nt;
     CUDA_TRY(h, cudaEventRecord(h->ev[0], st));
     k_init_iterate<<<grid_for(N, h->sms), BLOCK, 0, st>>>(h->P.ns, h->P.nt, d_u0, d_guess, h->U);
@@ -709,6 +738,7 @@ static int explicit_window(pit_handle* h, int s0, int L, const double* d_U, cons
 // (norms); the default recurrence path has none.
 static int solve_product(pit_handle* h, const double* d_u0, const double* d_bc, double* d_u_out, double* d_hist,
                          int* d_info, cudaStream_t st) {
+    NvtxRange nvtx_("product form (b2/N3) Newton loop");
     int rc = ensure_pf_scratch(h);
     if (rc != PIT_OK) return rc;
     const Prob& P = h->P;
@@ -789,6 +819,7 @@ static bool want_product(pit_handle* h, const double* d_bc, cudaStream_t st) {
 // The paper's initial iterate (pit_guess.cuh), written into iterate buffer 0.  Iterate
 // buffers 1 and 2 are free before the Newton launch and serve as the interpolation scratch (B >= 3).
 static int build_guess(pit_handle* h, const double* d_u0, const double* d_bc, cudaStream_t st) {
+    NvtxRange nvtx_("coarse-grid guess (N1)");
     GuessParams g = h->gp;
     const Prob& P = h->P;
     const long long N = P.ns * P.nt;
@@ -823,8 +854,13 @@ static int build_guess(pit_handle* h, const double* d_u0, const double* d_bc, cu
         return PIT_OK;
     };
     long long cl = 0;
-    const char* genv = getenv("PIT_GUESS_GRAPH");
-    const bool use_graph = !(genv && atoi(genv) == 0);
+    const bool use_graph = h->dbg.guess_graph;
+    // the graph bakes in whether coarse rings are passed: recapture when that changes between calls
+    const int ring_now = g.cring ? 1 : 0;
+    if (h->c_march && h->c_march_ring != ring_now) {
+        cudaGraphExecDestroy(h->c_march);
+        h->c_march = nullptr;
+    }
     if (use_graph && !h->c_march) {
         cudaStream_t cs = nullptr;
         cudaGraph_t graph = nullptr;
@@ -841,6 +877,7 @@ static int build_guess(pit_handle* h, const double* d_u0, const double* d_bc, cu
         if (!ok) { if (h->c_march) cudaGraphExecDestroy(h->c_march); h->c_march = nullptr; }
         cudaGetLastError();
         h->c_march_launches = ccl;
+        h->c_march_ring = ring_now;
     }
     if (use_graph && h->c_march) {
         CUDA_TRY(h, cudaGraphLaunch(h->c_march, st));
@@ -871,6 +908,7 @@ static int build_guess(pit_handle* h, const double* d_u0, const double* d_bc, cu
 
 int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, const double* d_guess, double* d_u_out,
                      double* d_hist, int32_t* d_info, void* cuda_stream) {
+    NvtxRange nvtx_("pit_solve_device");
     if (!h || !d_u0 || !d_u_out) return set_err(h, PIT_EINVAL, "null argument");
     CUDA_TRY(h, cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -908,6 +946,7 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
 int pit_slab_iterate_device(pit_handle* h, const double* d_uprev, const double* d_carry_in, const double* d_bc,
                             const double* d_U_k, double* d_U_k1, double* d_carry_out, double* d_hist, int32_t* d_info,
                             void* cuda_stream) {
+    NvtxRange nvtx_("pit_slab_iterate_device (N4)");
     if (!h || !d_uprev || !d_U_k || !d_U_k1 || !d_hist) return set_err(h, PIT_EINVAL, "null argument");
     if (!h->nb) return set_err(h, PIT_EINVAL, "time-slab iterations need engine 4 (pit_config.engine)");
     if (((uintptr_t)d_uprev | (uintptr_t)d_U_k | (uintptr_t)d_U_k1 | (uintptr_t)d_carry_in | (uintptr_t)d_carry_out) % 16)
@@ -938,6 +977,7 @@ int pit_initial_guess_device(pit_handle* h, const double* d_u0, const double* d_
 
 int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* guess, double* u_out, double* hist,
               int32_t* n_iter) {
+    NvtxRange nvtx_("pit_solve");
     if (!h || !u0 || !u_out) return set_err(h, PIT_EINVAL, "null argument");
     CUDA_TRY(h, cudaSetDevice(h->device));
     const Prob& P = h->P;
@@ -945,11 +985,20 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     CUDA_TRY(h, cudaMemcpy(h->d_u0, u0, sizeof(double) * P.ns, cudaMemcpyHostToDevice));
     const bool has_bc = P.bc == PIT_DIRICHLET && bc;
     if (has_bc) CUDA_TRY(h, cudaMemcpy(h->d_bc, bc, sizeof(double) * P.nt * P.ring_len, cudaMemcpyHostToDevice));
-    // the guess is staged straight into iterate buffer 0 (k_init_iterate then copies it in place)
+    // the guess is staged straight into iterate buffer 0 (k_init_iterate then copies it in place); without a guess
+    // a guess_cf handle builds the paper's coarse-grid guess there, as pit_solve_device does
     if (guess) CUDA_TRY(h, cudaMemcpy(h->U, guess, sizeof(double) * N, cudaMemcpyHostToDevice));
     h->launches = 0;
-    int rc = launch_init(h, h->d_u0, guess ? h->U : nullptr, 0);
-    if (rc != PIT_OK) return rc;
+    h->guess_timed = false;
+    int rc;
+    if (!guess && h->coarse) {
+        if ((rc = build_guess(h, h->d_u0, has_bc ? h->d_bc : nullptr, 0)) != PIT_OK) return rc;
+        CUDA_TRY(h, cudaEventRecord(h->ev[0], 0));
+        CUDA_TRY(h, cudaEventRecord(h->ev[1], 0));
+        h->timed = true;
+    } else if ((rc = launch_init(h, h->d_u0, guess ? h->U : nullptr, 0)) != PIT_OK) {
+        return rc;
+    }
     CUDA_TRY(h, cudaMemset(h->hist, 0, sizeof(double) * 4 * h->cfg.newton_max));
     h->product_used = 0;
     const bool prod = want_product(h, has_bc ? h->d_bc : nullptr, 0);
@@ -979,6 +1028,7 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
 
 int pit_residual_device(pit_handle* h, const double* d_U, const double* d_u0, const double* d_bc, double* d_R,
                         double* d_diag, double* d_norms, void* cuda_stream) {
+    NvtxRange nvtx_("pit_residual_device (kernel a)");
     if (!h || !d_U || !d_u0 || !d_R) return set_err(h, PIT_EINVAL, "null argument");
     CUDA_TRY(h, cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)cuda_stream;

@@ -101,3 +101,47 @@ def test_host_path_with_coarse_guess():
         s.close()
     assert st in (0, 1)
     assert normwise_rel(U, O.solve_sequential(p).U) <= 1e-10
+
+
+@pytest.mark.parametrize("case", ["periodic", "dirichlet_ring_then_null", "dirichlet_null_then_ring"])
+def test_guess_handle_reused_matches_fresh_handle(case):
+    """the coarse-march CUDA graph is captured once per handle; a second solve on the same handle (and a
+    change of ring presence between calls) must give the U, n_iter and hist of a fresh handle."""
+    torch = torch_cuda()
+    p, cf = (W.config(2, n=48, nt=12), 3) if case == "periodic" else (W.paper_heat(64, nt=8), 4)
+    rings = {"periodic": [None, None], "dirichlet_ring_then_null": [p.ring, None],
+             "dirichlet_null_then_ring": [None, p.ring]}[case]
+
+    def run(s, ring):
+        d_out = torch.empty((p.nt, p.ns), dtype=torch.float64, device="cuda")
+        d_hist = torch.zeros((s.cfg.newton_max, 4), dtype=torch.float64, device="cuda")
+        d_info = torch.zeros(2, dtype=torch.int32, device="cuda")
+        s.solve_device(dev(p.u0), None if ring is None else dev(ring), None, d_out, d_hist, d_info)
+        torch.cuda.synchronize()
+        n = int(d_info[0])
+        return d_out.cpu().numpy(), d_hist.cpu().numpy()[:n], n
+    s = pit.Solver(p, guess_cf=cf)
+    try:
+        first = run(s, rings[0])
+        second = run(s, rings[1])
+    finally:
+        s.close()
+    for got, ring in ((first, rings[0]), (second, rings[1])):
+        f = pit.Solver(p, guess_cf=cf)
+        try:
+            ref = run(f, ring)
+        finally:
+            f.close()
+        assert got[2] == ref[2]
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+
+
+def test_host_path_builds_the_coarse_guess():
+    """pit_solve (host buffers) with a guess_cf handle starts from the coarse-grid guess like
+    pit_solve_device: same n_iter and hist."""
+    p = W.paper_heat(64, nt=8)
+    U_d, h_d, n_d, s_d, _ = gpu_solve(p, guess_cf=4)
+    U_h, h_h, n_h, s_h = pit.solve(p, guess_cf=4)
+    assert n_h == n_d and np.array_equal(h_h, h_d) and np.array_equal(U_h, U_d)
+    U0, h0, n0, s0, _ = gpu_solve(p)                   # the u^0 start needs more iterations (paper's point)
+    assert n0 > n_d

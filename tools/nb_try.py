@@ -54,7 +54,7 @@ def main():
     if mode == "trace":
         import os
         os.environ["PIT_TRACE"] = "1"
-        for c, dd in ((5, 2), (5, 0), (4, 0), (3, 0), (2, 0)):
+        for c, dd in ((5, 3), (5, 0), (4, 0), (3, 0), (2, 0)):
             p = W.config(c)
             U, hist, nit, st, ms, ei, stt = run(p, reps=2, engine=4, pipeline_depth=dd)
             tm = {k: round(v / 1965.0, 1) for k, v in ei.get("trace_mean", {}).items()}
