@@ -21,6 +21,7 @@
 #include "pit_guess.cuh"
 #include "pit_explicit.cuh"
 #include "pit_nb_params.cuh"
+#include "pit_ps_params.cuh"
 
 using namespace pit;
 
@@ -88,6 +89,13 @@ struct pit_handle {
     unsigned long long* nb_qbits = nullptr;
     double* nb_ctl = nullptr;     // [4] omega, sweeps, q
     double* nb_linres = nullptr;  // [MAXK][2]
+    // engine 5 (pipeline of CTA sets, strips on chip, pit_newton_ps.cuh)
+    bool ps = false;              // the Newton solve runs on engine 5
+    int ps_D = 0, ps_Gs = 0, ps_he = 0, ps_threads = 0;   // CTA sets, strips per set, base strip height, threads per CTA
+    size_t ps_smem = 0;
+    unsigned long long* ps_llx = nullptr;   // [D][Gs][PS_RX][2][nxu / 2] LL cells
+    unsigned* ps_lvl = nullptr;             // [D][Gs] level counters
+    size_t ps_llx_bytes = 0;
     int last_engine = 0;          // engine of the last Newton solve
     // developer switches (pit.h "Debug environment"), read once at pit_create so a handle never changes path
     struct {
@@ -184,7 +192,7 @@ static int validate(const pit_config* c, char* why, size_t n) {
     }
     if (c->pipeline_depth < 0 || c->pipeline_depth > MAXD) { snprintf(why, n, "pipeline_depth must be in 0..%d", MAXD); return PIT_EINVAL; }
     if (c->window < 0) { snprintf(why, n, "window < 0"); return PIT_EINVAL; }
-    if (c->engine < 0 || c->engine > 4) { snprintf(why, n, "engine %d", c->engine); return PIT_EINVAL; }
+    if (c->engine < 0 || c->engine > 5) { snprintf(why, n, "engine %d", c->engine); return PIT_EINVAL; }
     if (c->lin_sweeps < 0 || c->lin_sweeps > 400) { snprintf(why, n, "lin_sweeps must be in 0..400"); return PIT_EINVAL; }
     if (c->lin_check < 0) { snprintf(why, n, "lin_check < 0"); return PIT_EINVAL; }
     if (c->stop_norm < 0 || c->stop_norm > 1) { snprintf(why, n, "stop_norm %d", c->stop_norm); return PIT_EINVAL; }
@@ -206,6 +214,8 @@ static void free_all(pit_handle* h) {
     dfree(h, h->ex_B); dfree(h, h->ex_C5); dfree(h, h->ex_err);
     dfree(h, h->nb_llx); dfree(h, h->nb_llu); dfree(h, h->nb_hpart); dfree(h, h->nb_sync); dfree(h, h->nb_qbits);
     dfree(h, h->nb_ctl); dfree(h, h->nb_linres);
+    dfree(h, h->ps_llx); dfree(h, h->ps_lvl);
+    h->ps_llx = nullptr; h->ps_lvl = nullptr;
     h->nb_llx = h->nb_llu = nullptr; h->nb_hpart = h->nb_ctl = h->nb_linres = nullptr; h->nb_sync = nullptr;
     h->nb_qbits = nullptr;
     h->ex_B = h->ex_C5 = nullptr; h->ex_err = nullptr; h->ex_capB = h->ex_capC = 0;
@@ -485,8 +495,40 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
         cudaGetLastError();
     }
     if (c.engine == 4 && !h->nb) { delete h; return PIT_EINVAL; }
+    // Engine 5 (the Newton solve): constant-viscosity Burgers on periodic grids, rows of 512 unknowns; D CTA sets of Gs
+    // strips with HE or HE + 2 rows each (HE even: every strip starts on an even row).  D = pipeline_depth, or the
+    // largest depth <= min(8, newton_max) whose strips fit on chip.
+    if ((c.engine == 0 || c.engine == 5) && (c.inverse_mode == PIT_INV_AUTO || c.inverse_mode == PIT_INV_RECURRENCE) &&
+        law == 1 && c.bc == PIT_PERIODIC && P.nyu % 2 == 0) {
+        const int dmax = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : 8, c.newton_max));
+        for (int D5 = dmax; D5 >= 1 && !h->ps; --D5) {
+            for (int Gs = std::min(h->sms / D5, P.nyu / 2); Gs >= 1 && !h->ps; --Gs) {
+                const int he = 2 * (P.nyu / (2 * Gs));
+                const int na = (P.nyu - he * Gs) / 2;          // strips with he + 2 rows
+                if (he < 2 || na < 0 || na > Gs) continue;
+                size_t smem5 = 0;
+                int thr5 = 0, occ5 = 0, he_used = he;
+                const void* fn = ps_kernel_law1(P.nxu, he, &smem5, &thr5);
+                if (!fn && na == 0 && he >= 4) {      // every strip has he rows = (he - 2) + 2
+                    he_used = he - 2;
+                    fn = ps_kernel_law1(P.nxu, he_used, &smem5, &thr5);
+                }
+                if (!fn || smem5 > 227 * 1024) continue;
+                if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5) != cudaSuccess ||
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ5, fn, thr5, smem5) != cudaSuccess || occ5 < 1) {
+                    cudaGetLastError();
+                    continue;
+                }
+                h->ps = true; h->ps_D = D5; h->ps_Gs = Gs; h->ps_he = he_used; h->ps_threads = thr5; h->ps_smem = smem5;
+                break;       // the largest Gs of this depth only: fewer strips would only lengthen them
+            }
+            if (c.pipeline_depth > 0) break;
+        }
+        cudaGetLastError();
+    }
+    if (c.engine == 5 && !h->ps) { delete h; return PIT_EINVAL; }
     const int D = h->D;
-    h->B = std::max(std::max(3, D), h->nb ? h->nb_D + 1 : 0);
+    h->B = std::max(std::max(std::max(3, D), h->nb ? h->nb_D + 1 : 0), h->ps ? h->ps_D + 1 : 0);
 
     const long long N = P.ns * P.nt;
     if ((rc = dalloc(h, &h->U, (size_t)(h->B * N))) ||
@@ -502,10 +544,12 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
         (rc = dalloc(h, &h->d_bc, (size_t)(c.bc == PIT_DIRICHLET ? (long long)P.nt * P.ring_len : 1))) ||
         (rc = dalloc(h, &h->d_small, 2 * 1024 + 2)) ||
         (rc = dalloc(h, &h->bs, 1)) ||
-        (h->dbg.trace && (rc = dalloc(h, &h->trace, 13 + 13 * GMAX2))) ||
+        (h->dbg.trace && (rc = dalloc(h, &h->trace, 13 + 13 * GMAX2 + (h->ps ? (size_t)h->ps_D * h->ps_Gs * PS_TR : 0)))) ||
         (h->nb && ((rc = dalloc(h, &h->nb_llx, (size_t)h->nb_G * h->nb_dm * NB_RX * 2 * (P.nxu / 2) * 2)) ||
-                   (rc = dalloc(h, &h->nb_llu, (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2)) ||
-                   (rc = dalloc(h, &h->nb_hpart, (size_t)MAXK * h->nb_G * NB_NP)) ||
+                   (rc = dalloc(h, &h->nb_llu, (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2)))) ||
+        (h->ps && ((rc = dalloc(h, &h->ps_llx, (size_t)h->ps_D * h->ps_Gs * PS_RX * 2 * (P.nxu / 2) * 2)) ||
+                   (rc = dalloc(h, &h->ps_lvl, (size_t)h->ps_D * h->ps_Gs)))) ||
+        ((h->nb || h->ps) && ((rc = dalloc(h, &h->nb_hpart, (size_t)MAXK * std::max(h->nb_G, h->ps_Gs) * NB_NP)) ||
                    (rc = dalloc(h, &h->nb_sync, (size_t)2 * MAXK)) ||
                    (rc = dalloc(h, &h->nb_qbits, 1)) ||
                    (rc = dalloc(h, &h->nb_ctl, 4)) ||
@@ -516,6 +560,7 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
     }
     h->nb_llx_bytes = (size_t)h->nb_G * h->nb_dm * NB_RX * 2 * (P.nxu / 2) * 2 * sizeof(unsigned long long);
     h->nb_llu_bytes = (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2 * sizeof(unsigned long long);
+    h->ps_llx_bytes = (size_t)h->ps_D * h->ps_Gs * PS_RX * 2 * (P.nxu / 2) * 2 * sizeof(unsigned long long);
     bool ev_ok = true;
     for (auto& e : h->ev) ev_ok = ev_ok && cudaEventCreate(&e) == cudaSuccess;
     if (!ev_ok || (!measure && (cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess ||
@@ -705,6 +750,44 @@ static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, doub
     CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
     h->launches += 9;
     h->last_engine = 4;
+    return PIT_OK;
+}
+
+// Engine 5: omega and the sweep count as engine 4 (k_nb_q / k_nb_ctl), then the persistent pipeline-of-sets kernel.
+static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double* d_hist, int* d_info, cudaStream_t st) {
+    NvtxRange nvtx_("engine5 k_newton_ps");
+    const Prob& P = h->P;
+    CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
+    CUDA_TRY(h, cudaMemsetAsync(h->ps_llx, 0, h->ps_llx_bytes, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->ps_lvl, 0, sizeof(unsigned) * h->ps_D * h->ps_Gs, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_sync, 0, sizeof(unsigned) * 2 * MAXK, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_linres, 0, sizeof(double) * 2 * MAXK, st));
+    CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
+    CUDA_TRY(h, cudaMemsetAsync(h->nb_qbits, 0, sizeof(unsigned long long), st));
+    nb_setup_launch(P, h->U, nullptr, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
+                    std::max(1, std::min(grid_for(P.ns, h->sms), 2 * h->sms)), st);
+    CUDA_TRY(h, cudaGetLastError());
+    PsParams S;
+    std::memset(&S, 0, sizeof(S));
+    S.P = P; S.u0 = d_u0; S.U = h->U; S.B = h->B; S.D = h->ps_D; S.Gs = h->ps_Gs;
+    S.ctl = h->nb_ctl; S.llx = h->ps_llx; S.lvl = h->ps_lvl; S.hpart = h->nb_hpart;
+    S.arrive = h->nb_sync; S.decided = h->nb_sync + MAXK;
+    S.hist = d_hist ? d_hist : h->hist; S.linres = h->nb_linres; S.info = d_info ? d_info : h->info;
+    S.u_out = d_u_out; S.newton_tol = h->cfg.newton_tol; S.newton_max = h->cfg.newton_max;
+    S.stop_norm = h->cfg.stop_norm;
+    S.stats = h->stats;
+    S.trace = h->trace ? h->trace + 13 + 13 * GMAX2 : nullptr;
+    S.ax = P.dt * P.i2hx; S.bx = P.dt * P.m0 * P.ihx2; S.ay = P.dt * P.i2hy; S.by = P.dt * P.m0 * P.ihy2;
+    S.aC1 = 1.0 + 2.0 * (S.bx + S.by); S.invC1 = 1.0 / S.aC1;
+    void* args[] = {(void*)&S};
+    size_t smem5 = 0;
+    int thr5 = 0;
+    const void* fn = ps_kernel_law1(P.nxu, h->ps_he, &smem5, &thr5);
+    CUDA_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ps_smem));
+    CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->ps_D * h->ps_Gs), dim3(h->ps_threads), args, h->ps_smem, st));
+    CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
+    h->launches += 9;
+    h->last_engine = 5;
     return PIT_OK;
 }
 
@@ -930,6 +1013,7 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
         CUDA_TRY(h, cudaMemcpyAsync(h->d_u0, d_u0, sizeof(double) * h->P.ns, cudaMemcpyDeviceToDevice, st));
         d_u0 = h->d_u0;
     }
+    if (h->ps) return launch_ps(h, d_u0, d_u_out, d_hist, (int*)d_info, st);
     if (h->nb) return launch_nb(h, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_u_out, d_hist, (int*)d_info, st);
     SolveParams S = base_params(h);
     S.u0 = d_u0;
@@ -1004,6 +1088,8 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     const bool prod = want_product(h, has_bc ? h->d_bc : nullptr, 0);
     if (prod) {
         rc = solve_product(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
+    } else if (h->ps) {
+        rc = launch_ps(h, h->d_u0, nullptr, h->hist, h->info, 0);
     } else if (h->nb) {
         rc = launch_nb(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else {
@@ -1226,18 +1312,20 @@ int pit_engine_info(pit_handle* h, double* out, int32_t n) {
     CUDA_TRY(h, cudaSetDevice(h->device));
     std::vector<double> v((size_t)4 + 2 * MAXK + 2 * NB_TR, 0.0);
     v[0] = h->last_engine ? h->last_engine : h->engine;
-    if (h->last_engine == 4) {
+    if (h->last_engine == 4 || h->last_engine == 5) {
         double ctl[3];
         CUDA_TRY(h, cudaMemcpy(ctl, h->nb_ctl, sizeof(ctl), cudaMemcpyDeviceToHost));
         v[1] = ctl[0]; v[2] = ctl[1]; v[3] = ctl[2];
         CUDA_TRY(h, cudaMemcpy(v.data() + 4, h->nb_linres, sizeof(double) * 2 * MAXK, cudaMemcpyDeviceToHost));
         if (h->trace) {   // cycle accounts: mean and max over CTAs (PIT_TRACE builds of the handle)
-            std::vector<unsigned long long> tr((size_t)h->nb_G * NB_TR);
-            CUDA_TRY(h, cudaMemcpy(tr.data(), h->trace + 13, tr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            static_assert(PS_TR == NB_TR, "one trace layout");
+            const int ng = h->last_engine == 5 ? h->ps_D * h->ps_Gs : h->nb_G;
+            std::vector<unsigned long long> tr((size_t)ng * NB_TR);
+            CUDA_TRY(h, cudaMemcpy(tr.data(), h->trace + 13 + (h->last_engine == 5 ? 13 * GMAX2 : 0), tr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
             for (int i = 0; i < NB_TR; ++i) {
                 double sum = 0, mx = 0;
-                for (int g = 0; g < h->nb_G; ++g) { sum += (double)tr[(size_t)g * NB_TR + i]; mx = std::max(mx, (double)tr[(size_t)g * NB_TR + i]); }
-                v[4 + 2 * MAXK + i] = sum / h->nb_G;
+                for (int g = 0; g < ng; ++g) { sum += (double)tr[(size_t)g * NB_TR + i]; mx = std::max(mx, (double)tr[(size_t)g * NB_TR + i]); }
+                v[4 + 2 * MAXK + i] = sum / ng;
                 v[4 + 2 * MAXK + NB_TR + i] = mx;
             }
         }

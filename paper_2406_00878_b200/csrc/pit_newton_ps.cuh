@@ -1,0 +1,515 @@
+// pit_newton_ps.cuh — engine 5: the all-at-once Newton solve (Eq. (5)) with the exact block inverse
+// of Eq. (7) applied as the level recurrence du^n = A_n^{-1}(r^n + du^{n-1}), as a PIPELINE OF CTA
+// SETS: set p (Gs CTAs, one per SM) runs Newton iteration k = pass * D + p over the levels n = 1..nt, one level
+// behind set p - 1, so D Newton iterations are in flight on D * Gs SMs (the level wavefront of DESIGN.md §6.1 laid
+// out in space instead of interleaved in every CTA as in engine 4).
+//
+// Per level a CTA holds its strip of H rows (c5: 22 rows of 512) ENTIRELY on chip: du (x) in registers (a thread owns
+// two adjacent columns of every strip row), u^n (with its two halo rows) and the right-hand side b = r^n + du^{n-1}
+// in shared memory.  HBM/L2 traffic per (level, iteration): U_k^n read once (into registers, issued before the
+// previous level's epilogue; u^{n-1} is still in shared memory from the previous level) and U_{k+1}^n written once —
+// the 16 B per DOF per Newton iteration of SURVEY §8(d).
+//
+// Level solves: S red-black SOR sweeps from the carry, Young's omega from the Jacobi bound (as engine 4, whose
+// device set-up kernels k_nb_q / k_nb_ctl are reused).  A half-sweep first turns every point of the OTHER colour into
+// its four products with the coefficients its neighbours apply to it (one load of u, seven flops) and scatters them
+// into per-row accumulators, so every value of u and x is touched once per half-sweep.  Synchronisation:
+// neighbouring strips of a set exchange their boundary rows through LL cells (no fences, pit_newton_nb.cuh) once per
+// half-sweep — the loads are issued before the strip's own products and consumed after them, boundary rows are
+// relaxed and published first; set p - 1 hands U_k^n to set p through per-strip level counters (release / acquire)
+// that thread 0 publishes and polls where it would wait for its neighbours anyway.  Columns of neighbouring threads
+// meet through warp shuffles (warp edges through a small shared array).
+//
+// This engine covers LAW 1 (viscous Burgers, constant viscosity) on periodic grids with an even number of rows per
+// strip; everything else runs on engines 1-4.
+#pragma once
+#include "pit_newton_nb.cuh"
+#include "pit_ps_params.cuh"
+
+namespace pit {
+
+namespace ps {
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_rlx(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+}  // namespace ps
+
+template <int NXU, int HE>
+struct PsEngine {
+    static constexpr int T = NXU / 2;          // threads per CTA (two columns each)
+    static constexpr int NW = T / 32;          // warps
+    static constexpr int NTH = T;
+    static constexpr int HM = HE + 2;          // max strip height (strips have HE or HE + 2 rows, r0 even)
+    static constexpr size_t OFF_U = 0;                                    // ubuf [HM + 2][NXU]: u^n rows r0-1 .. r0+H
+    static constexpr size_t OFF_B = OFF_U + (size_t)(HM + 2) * NXU;       // bs   [HM][2][T]
+    static constexpr size_t OFF_A = OFF_B + (size_t)HM * 2 * T;           // acc  [NB_NP][T] per-thread norm partials
+    static constexpr size_t OFF_E = OFF_A + (size_t)NB_NP * T;            // wedge [2][HM][NW] warp-edge E/W products
+    static constexpr size_t OFF_R = OFF_E + (size_t)2 * HM * NW;          // red  [NW][NB_NP]
+    static constexpr size_t SMEM = (OFF_R + (size_t)NW * NB_NP) * sizeof(double);
+
+    template <int H>
+    __device__ __forceinline__ static void run(const PsParams& S, double* sm) {
+        const Prob P = S.P;
+        const int Gs = S.Gs, c = blockIdx.x, p = c / Gs, s = c % Gs;
+        const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+        const int nyu = P.nyu, nt = P.nt, D = S.D, B = S.B;
+        const long long ns = P.ns;
+        const int na = (nyu - HE * Gs) / 2;                 // strips 0 .. na-1 have HE + 2 rows
+        const int r0 = s * HE + 2 * min(s, na);             // first own row (even)
+        const int ss = s > 0 ? s - 1 : Gs - 1, sn = s + 1 < Gs ? s + 1 : 0;   // periodic neighbours (rows below / above)
+        const int rS = (r0 - 1 + nyu) % nyu, rN = (r0 + H) % nyu;
+
+        double* ubuf = sm + OFF_U;
+        double* bs = sm + OFF_B;
+        double* accs = sm + OFF_A;
+        double* wedgeW = sm + OFF_E;                         // [HM][NW] W products for lane 0 of warp w + 1
+        double* wedgeE = wedgeW + (size_t)HM * NW;           // [HM][NW] E products for lane 31 of warp w - 1
+        double* red_s = sm + OFF_R;
+        __shared__ int s_dec[2];
+        __shared__ int s_last;
+        __shared__ volatile int s_pf;                        // level whose U_k rows set p-1 has published (thread 0)
+        __shared__ long long s_tr[PS_TR];
+
+        unsigned long long* myx = S.llx + ((size_t)(p * Gs + s) * PS_RX * 2 * T) * 2;
+        const unsigned long long* sx = S.llx + ((size_t)(p * Gs + ss) * PS_RX * 2 * T) * 2;
+        const unsigned long long* nxq = S.llx + ((size_t)(p * Gs + sn) * PS_RX * 2 * T) * 2;
+
+        const int t = tid, c0 = 2 * t;
+        const double omega = __ldcg(S.ctl);
+        const int SW = (int)__ldcg(S.ctl + 1);
+        const int chk = max(1, (int)__ldcg(S.ctl + 3));
+#define ax (S.ax)
+#define bx (S.bx)
+#define ay (S.ay)
+#define by (S.by)
+#define aC1 (S.aC1)
+#define tau (S.P.dt)
+        const double oic = omega * S.invC1, om1 = 1.0 - omega;     // x <- om1 x + oic (b - offdiag x)
+        const int wp = (w + NW - 1) % NW, wn = (w + 1) % NW;
+        const int cW = (c0 + NXU - 1) & (NXU - 1), cE = (c0 + 2) & (NXU - 1);
+
+        auto cbar = [&]() { __syncthreads(); };
+        auto bsm = [&](int r, int j) -> double& { return bs[(size_t)(r * 2 + j) * T + t]; };
+        auto ac = [&](int j) -> double& { return accs[(size_t)j * T + t]; };
+        auto xcell = [&](auto* base, unsigned q, int side) { return base + ((size_t)((q % PS_RX) * 2 + side) * T + t) * 2; };
+
+        double x[H][2];
+        #pragma unroll
+        for (int j = 0; j < NB_NP; ++j) accs[(size_t)j * T + tid] = 0.0;
+        int lastx = -1;
+        unsigned qx = 0;
+        int levels = 0;
+        if (tid == 0) s_pf = 0;
+        const bool trace = S.trace != nullptr && t == 0;     // cycle accounts of thread 0, kept in shared memory
+        if (trace) for (int i = 0; i < PS_TR; ++i) s_tr[i] = 0;
+        __shared__ long long s_tm[2];
+        if (trace) s_tm[0] = s_tm[1] = clock64();
+        auto mark = [&](int i) { if (trace) { const long long now = clock64(); s_tr[i] += now - s_tm[1]; s_tm[1] = now; } };
+        auto take = [&](const unsigned long long* q, LLc cl, unsigned f) -> double {
+            if (trace) {
+                long long a = 0;
+                const double v = ll_take_t(q, cl, f, a);
+                s_tr[3] += a;
+                return v;
+            }
+            return ll_take(q, cl, f);
+        };
+
+        // ---- thread 0's side jobs (no warp is set aside for them: a ninth warp would cap registers at 168) ----
+        const unsigned* fprev = p > 0 ? S.lvl + (size_t)(p - 1) * Gs : nullptr;   // set p-1's level counters
+        unsigned* fmine = S.lvl + (size_t)p * Gs + s;
+        int flag_lv = 0;        // thread 0: level whose U_{k+1} rows are written but not yet published (0 = none)
+        int pf_lv = 0;          // thread 0: level whose U_k rows (set p-1) are still to be confirmed (0 = none)
+        // One fence serves both jobs: it releases this strip's U_{k+1}^{flag_lv} rows (every thread stored them before
+        // the last CTA barrier) ahead of the level counter, and it orders set p-1's counters (relaxed loads) before this
+        // CTA's loads of their rows (which follow the next CTA barrier).
+        auto service = [&](unsigned base) {
+            unsigned v0 = 0xffffffffu, v1 = 0xffffffffu, v2 = 0xffffffffu;
+            if (pf_lv && fprev) { v0 = ps::ld_rlx(fprev + s); v1 = ps::ld_rlx(fprev + ss); v2 = ps::ld_rlx(fprev + sn); }
+            const bool ready = pf_lv && min(v0, min(v1, v2)) >= base + (unsigned)pf_lv;
+            if (flag_lv || (ready && fprev)) __threadfence();
+            if (flag_lv) {
+                asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(fmine), "r"(base + (unsigned)flag_lv) : "memory");
+                flag_lv = 0;
+            }
+            if (ready) {
+                s_pf = pf_lv;
+                pf_lv = 0;
+            }
+        };
+
+        // tt[q] = b - (off-diagonal part of A_n) x at the colour-cc point of every row q (column j_q = (q + cc) & 1).
+        // Every point of the other colour (q, 1 - j_q) is turned into its products with the coefficients its four
+        // neighbours apply to it: a_E = ax u - bx (seen from its W neighbour), a_W = -ax u - bx, a_N = ay u - by (seen
+        // from the row below), a_S = -ay u - by.  The product for the neighbouring THREAD travels by warp shuffle (warp
+        // edges through shared memory); the neighbouring strips' rows arrive in LL cells.
+        auto gather = [&](const int cc, double (&tt)[H], const bool svc, const unsigned fbase) {
+            LLc hs, hn;
+            const unsigned qn = (unsigned)lastx;
+            if (lastx >= 0) {
+                hs = ll_issue(xcell(sx, qn, 1));
+                hn = ll_issue(xcell(nxq, qn, 0));
+            }
+            if (svc && t == 0 && (flag_lv | pf_lv)) service(fbase);
+            double oq[H];
+            #pragma unroll
+            for (int q = 0; q < H; ++q) tt[q] = bsm(q, (q + cc) & 1);
+            #pragma unroll
+            for (int q = 0; q < H; ++q) {
+                const int jn = 1 - ((q + cc) & 1);               // the other colour's column of this row
+                const double uq = ubuf[(size_t)(q + 1) * NXU + c0 + jn], xq = x[q][jn];
+                const double m = uq * xq, bxq = bx * xq, byq = by * xq;
+                const double eq = fma(ax, m, -bxq), wq = fma(-ax, m, -bxq);
+                if (jn == 1) { tt[q] -= eq; oq[q] = wq; } else { tt[q] -= wq; oq[q] = eq; }
+                if (q > 0) tt[q > 0 ? q - 1 : 0] -= fma(ay, m, -byq);
+                if (q + 1 < H) tt[q + 1 < H ? q + 1 : q] -= fma(-ay, m, -byq);
+                if (jn == 1) { if (lane == 31) wedgeW[q * NW + w] = wq; }
+                else { if (lane == 0) wedgeE[q * NW + w] = eq; }
+            }
+            cbar();
+            #pragma unroll
+            for (int q = 0; q < H; ++q) {
+                const int jn = 1 - ((q + cc) & 1);
+                double in;
+                if (jn == 1) {       // active column 0: W neighbour = thread t-1's column 1
+                    in = __shfl_up_sync(0xffffffffu, oq[q], 1);
+                    const double e = wedgeW[q * NW + wp];
+                    in = lane == 0 ? e : in;
+                } else {             // active column 1: E neighbour = thread t+1's column 0
+                    in = __shfl_down_sync(0xffffffffu, oq[q], 1);
+                    const double e = wedgeE[q * NW + wn];
+                    in = lane == 31 ? e : in;
+                }
+                tt[q] -= in;
+            }
+            if (lastx >= 0) {        // the neighbouring strips' boundary rows (their last publication: the other colour)
+                const double xs_h = take(xcell(sx, qn, 1), hs, qn + 1u);
+                const double xn_h = take(xcell(nxq, qn, 0), hn, qn + 1u);
+                const double uS = ubuf[c0 + (cc & 1)], uN = ubuf[(size_t)(H + 1) * NXU + c0 + ((H - 1 + cc) & 1)];
+                tt[0] = fma(-fma(-ay, uS, -by), xs_h, tt[0]);
+                tt[H - 1] = fma(-fma(ay, uN, -by), xn_h, tt[H - 1]);
+            }
+        };
+
+        for (int pass = 0;; ++pass) {
+            const int k = pass * D + p;
+            const bool active = p < D && k < S.newton_max;
+            const double* Uk = S.U + (size_t)(k % B) * nt * ns;
+            const unsigned fbase = (unsigned)pass * (unsigned)nt;
+            double2 pf[H + 2];                                   // u^n rows r0-1 .. r0+H of the level about to start
+            auto load_pf = [&](int lv) {
+                const double* un = Uk + (size_t)(lv - 1) * ns;
+                pf[0] = ldcg2(un + (size_t)rS * NXU + c0);
+                #pragma unroll
+                for (int r = 0; r < H; ++r) pf[r + 1] = ldcg2(un + (size_t)(r0 + r) * NXU + c0);
+                pf[H + 1] = ldcg2(un + (size_t)rN * NXU + c0);
+            };
+            if (active) {
+                #pragma unroll
+                for (int r = 0; r < H; ++r) {
+                    x[r][0] = 0.0; x[r][1] = 0.0;
+                    *reinterpret_cast<double2*>(ubuf + (size_t)(r + 1) * NXU + c0) = ldcg2(S.u0 + (size_t)(r0 + r) * NXU + c0);   // u^{n-1} of level 1
+                }
+                lastx = -1;
+                if (t == 0) {
+                    pf_lv = 1;
+                    for (;;) {
+                        service(fbase);
+                        if (!pf_lv) break;
+                        __nanosleep(64);
+                    }
+                }
+                cbar();
+                load_pf(1);
+            }
+            for (int n = 1; active && n <= nt; ++n) {
+                ++levels;
+                mark(6);
+                // ---- prologue 1: b = du^{n-1} - (u^n - u^{n-1}); u^n replaces u^{n-1} in shared memory
+                #pragma unroll
+                for (int r = 0; r < H; ++r) {
+                    double2* up = reinterpret_cast<double2*>(ubuf + (size_t)(r + 1) * NXU + c0);
+                    const double2 old = *up;
+                    bsm(r, 0) = x[r][0] - (pf[r + 1].x - old.x);
+                    bsm(r, 1) = x[r][1] - (pf[r + 1].y - old.y);
+                    *up = pf[r + 1];
+                }
+                *reinterpret_cast<double2*>(ubuf + c0) = pf[0];
+                *reinterpret_cast<double2*>(ubuf + (size_t)(H + 1) * NXU + c0) = pf[H + 1];
+                cbar();
+                if (t == 0 && n < nt) pf_lv = n + 1;
+                mark(0);
+                // ---- prologue 2: r^n = -G^n, b = r^n + du^{n-1}
+                {
+                    double ar2 = 0.0, arm = 0.0;
+                    #pragma unroll
+                    for (int r = 0; r < H; ++r) {
+                        const double2 prv = pf[r], cur = pf[r + 1], nxt = pf[r + 2];
+                        const double uw = ubuf[(size_t)(r + 1) * NXU + cW], ue = ubuf[(size_t)(r + 1) * NXU + cE];
+                        // column 0: W = uw, E = cur.y; column 1: W = cur.x, E = ue
+                        const double conv0 = 0.5 * ((cur.y * cur.y - uw * uw) * P.i2hx + (nxt.x * nxt.x - prv.x * prv.x) * P.i2hy);
+                        const double visc0 = P.m0 * ((cur.y - 2.0 * cur.x + uw) * P.ihx2 + (nxt.x - 2.0 * cur.x + prv.x) * P.ihy2);
+                        const double conv1 = 0.5 * ((ue * ue - cur.x * cur.x) * P.i2hx + (nxt.y * nxt.y - prv.y * prv.y) * P.i2hy);
+                        const double visc1 = P.m0 * ((ue - 2.0 * cur.y + cur.x) * P.ihx2 + (nxt.y - 2.0 * cur.y + prv.y) * P.ihy2);
+                        const double f0 = tau * (conv0 - visc0), f1 = tau * (conv1 - visc1);
+                        const double b0 = bsm(r, 0), b1 = bsm(r, 1);
+                        const double G0 = (x[r][0] - b0) + f0, G1 = (x[r][1] - b1) + f1;     // (u^n - u^{n-1}) + tau F(u^n)
+                        bsm(r, 0) = b0 - f0;
+                        bsm(r, 1) = b1 - f1;
+                        ar2 = fma(G0, G0, fma(G1, G1, ar2));
+                        arm = fmax(arm, fmax(fabs(G0), fabs(G1)));
+                    }
+                    ac(0) += ar2;
+                    ac(1) = fmax(ac(1), arm);
+                }
+                mark(1);
+                // ---- S red-black SOR sweeps, one neighbour exchange per half-sweep
+                const bool chkl = (n % chk == 0) || n == nt;
+                for (int m = 0; m < SW; ++m) {
+                    const bool lastm = m == SW - 1 && chkl;
+                    #pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        double tt[H];
+                        gather(cc, tt, true, fbase);
+                        double rs2 = 0.0, rsm = 0.0;
+                        #pragma unroll
+                        for (int i = 0; i < H; ++i) {
+                            const int r = i == 0 ? 0 : (i == 1 ? H - 1 : i - 1);     // boundary rows first
+                            const int j = (r + cc) & 1;
+                            const double xo = x[r][j];
+                            const double xn = fma(oic, tt[r], om1 * xo);
+                            x[r][j] = xn;
+                            if (cc == 1 && lastm) {
+                                const double rr = aC1 * (om1 / omega) * (xn - xo);
+                                rs2 = fma(rr, rr, rs2);
+                                rsm = fmax(rsm, fabs(rr));
+                            }
+                            if (i == (H > 1 ? 1 : 0)) {
+                                const unsigned f = qx + 1u;
+                                ll_put(xcell(myx, qx, 0), x[0][cc & 1], f);
+                                ll_put(xcell(myx, qx, 1), x[H - 1][(H - 1 + cc) & 1], f);
+                            }
+                        }
+                        if (cc == 1 && lastm) {
+                            ac(4) += rs2;
+                            ac(5) = fmax(ac(5), rsm);
+                        }
+                        lastx = (int)qx;
+                        ++qx;
+                    }
+                }
+                mark(2);
+                // ---- the next level's u rows (registers), if set p-1 has published them
+                bool pf_loaded = n == nt;
+                cbar();                                             // s_pf of the last service() calls
+                if (!chkl && !pf_loaded && s_pf == n + 1) { load_pf(n + 1); pf_loaded = true; }   // (not across the check: registers)
+                // ---- epilogue: U_{k+1}^n = U_k^n + du^n (du^n stays in x as the next carry)
+                {
+                    double* Un = S.U + (size_t)((k + 1) % B) * nt * ns + (size_t)(n - 1) * ns;
+                    double d2 = 0.0, dm = 0.0;
+                    #pragma unroll
+                    for (int r = 0; r < H; ++r) {
+                        double2 v = *reinterpret_cast<const double2*>(ubuf + (size_t)(r + 1) * NXU + c0);
+                        v.x += x[r][0];
+                        v.y += x[r][1];
+                        *reinterpret_cast<double2*>(Un + (size_t)(r0 + r) * NXU + c0) = v;
+                        d2 = fma(x[r][0], x[r][0], fma(x[r][1], x[r][1], d2));
+                        dm = fmax(dm, fmax(fabs(x[r][0]), fabs(x[r][1])));
+                    }
+                    ac(2) += d2;
+                    ac(3) = fmax(ac(3), dm);
+                    if (t == 0) flag_lv = n;                        // published by service() after the next CTA barrier
+                }
+                mark(4);
+                // ---- a-posteriori residual of the red points after the final black half-sweep
+                if (chkl) {
+                    double tt[H];
+                    gather(0, tt, false, fbase);
+                    double rs2 = 0.0, rsm = 0.0, bb2 = 0.0;
+                    #pragma unroll
+                    for (int r = 0; r < H; ++r) {
+                        const double rr = tt[r] - aC1 * x[r][r & 1];
+                        rs2 = fma(rr, rr, rs2);
+                        rsm = fmax(rsm, fabs(rr));
+                        bb2 = fma(bsm(r, 0), bsm(r, 0), fma(bsm(r, 1), bsm(r, 1), bb2));
+                    }
+                    ac(4) += rs2;
+                    ac(5) = fmax(ac(5), rsm);
+                    ac(6) += bb2;
+                    mark(5);
+                }
+                // ---- iteration end: per-CTA partials, the set's last CTA reduces and decides
+                if (n == nt) {
+                    double a[NB_NP];
+                    #pragma unroll
+                    for (int j = 0; j < NB_NP; ++j) {
+                        a[j] = ac(j);
+                        ac(j) = 0.0;
+                    }
+                    #pragma unroll
+                    for (int j = 0; j < NB_NP; ++j)
+                        #pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double y = __shfl_xor_sync(0xffffffffu, a[j], o);
+                            a[j] = nb_is_max(j) ? fmax(a[j], y) : a[j] + y;
+                        }
+                    if (lane == 0)
+                        #pragma unroll
+                        for (int j = 0; j < NB_NP; ++j) red_s[w * NB_NP + j] = a[j];
+                    cbar();
+                    if (t == 0) {
+                        service(fbase);                            // level nt's counter (fence inside)
+                        double* hp = S.hpart + ((size_t)k * Gs + s) * NB_NP;
+                        for (int j = 0; j < NB_NP; ++j) {
+                            double v = red_s[j];
+                            for (int ww = 1; ww < NW; ++ww) v = nb_is_max(j) ? fmax(v, red_s[ww * NB_NP + j]) : v + red_s[ww * NB_NP + j];
+                            hp[j] = v;
+                        }
+                        __threadfence();
+                        s_last = atomicAdd(S.arrive + k, 1u) == (unsigned)(Gs - 1);
+                    }
+                    cbar();
+                    if (s_last && t < 32) {
+                        __threadfence();
+                        double g4[NB_NP] = {0, 0, 0, 0, 0, 0, 0};
+                        for (int gg = t; gg < Gs; gg += 32) {
+                            const double* hp = S.hpart + ((size_t)k * Gs + gg) * NB_NP;
+                            #pragma unroll
+                            for (int j = 0; j < NB_NP; ++j) {
+                                const double v = __ldcg(hp + j);
+                                g4[j] = nb_is_max(j) ? fmax(g4[j], v) : g4[j] + v;
+                            }
+                        }
+                        #pragma unroll
+                        for (int j = 0; j < NB_NP; ++j)
+                            #pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) {
+                                const double y = __shfl_xor_sync(0xffffffffu, g4[j], o);
+                                g4[j] = nb_is_max(j) ? fmax(g4[j], y) : g4[j] + y;
+                            }
+                        if (t == 0) {
+                            const double Ntot = (double)ns * (double)nt;
+                            S.hist[4 * k + 0] = sqrt(g4[0] / Ntot);
+                            S.hist[4 * k + 1] = g4[1];
+                            S.hist[4 * k + 2] = sqrt(g4[2] / Ntot);
+                            S.hist[4 * k + 3] = g4[3];
+                            if (S.linres) {
+                                S.linres[2 * k + 0] = g4[6] > 0.0 ? sqrt(g4[4] / g4[6]) : 0.0;
+                                S.linres[2 * k + 1] = g4[5];
+                            }
+                            const double dn = S.stop_norm ? sqrt(g4[2] / Ntot) : g4[3];
+                            double prev = INFINITY;
+                            if (k >= 1) {
+                                while (*((volatile unsigned*)(S.decided + k - 1)) == 0) __nanosleep(64);
+                                __threadfence();
+                                prev = S.stop_norm ? __ldcg(S.hist + 4 * (k - 1) + 2) : __ldcg(S.hist + 4 * (k - 1) + 3);
+                            }
+                            int st = 2;
+                            bool finite = true;
+                            #pragma unroll
+                            for (int j = 0; j < NB_NP; ++j) finite = finite && isfinite(g4[j]);
+                            if (!finite) st = -5;
+                            else if (dn <= S.newton_tol) st = 0;
+                            else if (k >= 1 && dn > 0.5 * prev && dn <= 1e3 * S.newton_tol) st = 1;
+                            else if (k + 1 >= S.newton_max) st = -4;
+                            __threadfence();
+                            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(S.decided + k), "r"((unsigned)(16 + st)) : "memory");
+                        }
+                    }
+                }
+                // ---- (rare) set p-1 had not published the next level yet: wait for it, then load
+                if (!pf_loaded && s_pf == n + 1) { load_pf(n + 1); pf_loaded = true; }
+                while (!pf_loaded) {
+                    if (t == 0) {
+                        for (;;) {
+                            service(fbase);
+                            if (!pf_lv) break;
+                            __nanosleep(64);
+                        }
+                    }
+                    cbar();
+                    if (s_pf == n + 1) { load_pf(n + 1); pf_loaded = true; }
+                }
+                cbar();                                             // every thread is done reading this level's u
+            }
+            // ---- pass end: every set done; wait for the decisions of this pass's iterations
+            __syncthreads();          // (A)
+            const int kl = min(pass * D + D, S.newton_max) - 1;
+            if (tid == 0) {
+                unsigned v;
+                for (;;) {
+                    v = ps::ld_acq(S.decided + kl);
+                    if (v) break;
+                    __nanosleep(128);
+                }
+                int st = 2, kf = -1;
+                for (int kk = pass * D; kk <= kl; ++kk) {
+                    const int sk = (int)*((volatile unsigned*)(S.decided + kk)) - 16;
+                    if (sk != 2) { st = sk; kf = kk + 1; break; }
+                }
+                s_dec[0] = st;
+                s_dec[1] = kf;
+            }
+            __syncthreads();          // (B)
+            if (s_dec[0] != 2) break;
+        }
+        if (trace) {
+            s_tr[PS_TR - 1] = clock64() - s_tm[0];
+            for (int i = 0; i < PS_TR; ++i) S.trace[(size_t)c * PS_TR + i] = (unsigned long long)s_tr[i];
+        }
+        if (c == 0 && tid == 0) {
+            S.info[0] = s_dec[1];
+            S.info[1] = s_dec[0];
+            // speculative iterations past the deciding one leave no history
+            for (int kk = s_dec[1]; kk < S.newton_max && kk < MAXK && __ldcg(S.decided + kk) != 0u; ++kk) {
+                for (int j = 0; j < 4; ++j) S.hist[4 * kk + j] = 0.0;
+                if (S.linres) { S.linres[2 * kk] = 0.0; S.linres[2 * kk + 1] = 0.0; }
+            }
+            if (S.stats) {
+                S.stats[0] = levels; S.stats[1] = (long long)SW;
+                S.stats[2] = D; S.stats[3] = (long long)D * Gs; S.stats[4] = (long long)levels * SW; S.stats[5] = 0;
+            }
+        }
+        copy_out(S, s_dec[1]);
+#undef ax
+#undef bx
+#undef ay
+#undef by
+#undef aC1
+#undef tau
+    }
+
+    // The converged iterate (buffer kf % B) copied to u_out by every CTA of the grid.
+    __device__ __forceinline__ static void copy_out(const PsParams& S, int kf) {
+        if (!S.u_out) return;
+        const long long n2 = (long long)S.P.nt * S.P.ns / 2;
+        const double2* src = reinterpret_cast<const double2*>(S.U + (size_t)(kf % S.B) * S.P.nt * S.P.ns);
+        double2* dst = reinterpret_cast<double2*>(S.u_out);
+        const long long stride = (long long)S.D * S.Gs * NTH;
+        long long i = (long long)blockIdx.x * NTH + threadIdx.x;
+        for (; i + 3 * stride < n2; i += 4 * stride) {
+            const double2 a = __ldcg(src + i), b = __ldcg(src + i + stride), cc = __ldcg(src + i + 2 * stride), d = __ldcg(src + i + 3 * stride);
+            __stcs(dst + i, a); __stcs(dst + i + stride, b); __stcs(dst + i + 2 * stride, cc); __stcs(dst + i + 3 * stride, d);
+        }
+        for (; i < n2; i += stride) __stcs(dst + i, __ldcg(src + i));
+    }
+};
+
+template <int NXU, int HE>
+__global__ void __launch_bounds__(NXU / 2, 1) k_newton_ps(const PsParams S) {
+    extern __shared__ __align__(128) double sm_ps[];
+    using E = PsEngine<NXU, HE>;
+    if ((int)blockIdx.x >= S.D * S.Gs) return;
+    const int s = blockIdx.x % S.Gs;
+    const int na = (S.P.nyu - HE * S.Gs) / 2;
+    if (s < na) E::template run<HE + 2>(S, sm_ps); else E::template run<HE>(S, sm_ps);
+}
+
+}  // namespace pit

@@ -1,0 +1,20 @@
+// pit_ps_law1.cu — engine-5 instantiations (LAW 1: viscous Burgers, constant viscosity; periodic grids), compiled as
+// their own translation unit.
+#include "pit_newton_ps.cuh"
+
+namespace pit {
+
+template <int NXU, int HE>
+static const void* ps_inst(size_t* smem, int* threads) {
+    *smem = PsEngine<NXU, HE>::SMEM;
+    *threads = PsEngine<NXU, HE>::NTH;
+    return (const void*)k_newton_ps<NXU, HE>;
+}
+
+// Instantiated shapes: (row length, base strip height HE); a set's strips have HE or HE + 2 rows.
+const void* ps_kernel_law1(int nxu, int he, size_t* smem, int* threads) {
+    if (nxu == 512 && he == 20) return ps_inst<512, 20>(smem, threads);
+    return nullptr;
+}
+
+}  // namespace pit
