@@ -5,8 +5,8 @@
 // out in space instead of interleaved in every CTA as in engine 4).
 //
 // Per level a CTA holds its strip of H rows (c5: 22 rows of 512) ENTIRELY on chip: du (x) in registers (a thread owns
-// two adjacent columns of every strip row), u^n (with its two halo rows) and the right-hand side b = r^n + du^{n-1}
-// in shared memory.  HBM/L2 traffic per (level, iteration): U_k^n read once (into registers, issued before the
+// two adjacent columns of one half of the strip's rows: two row groups of NXU / 2 threads), u^n (with its two halo rows)
+// and the right-hand side b = r^n + du^{n-1} in shared memory.  HBM/L2 traffic per (level, iteration): U_k^n read once (into registers, issued before the
 // previous level's epilogue; u^{n-1} is still in shared memory from the previous level) and U_{k+1}^n written once —
 // the 16 B per DOF per Newton iteration of SURVEY §8(d).
 //
@@ -43,86 +43,109 @@ __device__ __forceinline__ unsigned ld_rlx(const unsigned* p) {
 
 template <int NXU, int HE>
 struct PsEngine {
-    static constexpr int T = NXU / 2;          // threads per CTA (two columns each)
-    static constexpr int NW = T / 32;          // warps
-    static constexpr int NTH = T;
+    static constexpr int T = NXU / 2;          // threads per row group (two columns each)
+    static constexpr int NW = T / 32;          // warps per row group
+    static constexpr int NTH = 2 * T;          // two row groups: the lower and the upper half of the strip's rows
     static constexpr int HM = HE + 2;          // max strip height (strips have HE or HE + 2 rows, r0 even)
+    static constexpr int HHM = HM / 2;         // max rows per thread
     static constexpr size_t OFF_U = 0;                                    // ubuf [HM + 2][NXU]: u^n rows r0-1 .. r0+H
-    static constexpr size_t OFF_B = OFF_U + (size_t)(HM + 2) * NXU;       // bs   [HM][2][T]
-    static constexpr size_t OFF_A = OFF_B + (size_t)HM * 2 * T;           // acc  [NB_NP][T] per-thread norm partials
-    static constexpr size_t OFF_E = OFF_A + (size_t)NB_NP * T;            // wedge [2][HM][NW] warp-edge E/W products
-    static constexpr size_t OFF_R = OFF_E + (size_t)2 * HM * NW;          // red  [NW][NB_NP]
-    static constexpr size_t SMEM = (OFF_R + (size_t)NW * NB_NP) * sizeof(double);
+    static constexpr size_t OFF_B = OFF_U + (size_t)(HM + 2) * NXU;       // bs   [HHM][2][NTH]
+    static constexpr size_t OFF_A = OFF_B + (size_t)HHM * 2 * NTH;        // acc  [NB_NP][NTH] per-thread norm partials
+    static constexpr size_t OFF_E = OFF_A + (size_t)NB_NP * NTH;          // wedge [2 groups][2 kinds][HHM][NW] warp-edge E/W products
+    static constexpr size_t OFF_G = OFF_E + (size_t)4 * HHM * NW;         // gx   [2 colours][2][T] N/S products across the row groups
+    static constexpr size_t OFF_R = OFF_G + (size_t)4 * T;                // red  [2 NW][NB_NP]
+    static constexpr size_t SMEM = (OFF_R + (size_t)2 * NW * NB_NP) * sizeof(double);
 
-    template <int H>
+    // HH = rows per thread (H = 2 HH rows per strip).  Row group g owns strip rows g HH .. g HH + HH - 1.  When HH is
+    // odd the upper group starts on an odd row: its threads hold their two columns SWAPPED (local column jj = actual
+    // column ^ f), so that the colour of local point (q, jj) is (q + jj) & 1 in both groups and every register
+    // subscript stays compile-time; the E/W roles then mirror, which only flips the sign of ax and the shuffle
+    // direction (per-thread constants).
+    template <int HH>
     __device__ __forceinline__ static void run(const PsParams& S, double* sm) {
+        constexpr int H = 2 * HH;
         const Prob P = S.P;
         const int Gs = S.Gs, c = blockIdx.x, p = c / Gs, s = c % Gs;
         const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+        const int g = tid / T, t = tid % T, wl = w % NW;
         const int nyu = P.nyu, nt = P.nt, D = S.D, B = S.B;
         const long long ns = P.ns;
         const int na = (nyu - HE * Gs) / 2;                 // strips 0 .. na-1 have HE + 2 rows
-        const int r0 = s * HE + 2 * min(s, na);             // first own row (even)
+        const int r0 = s * HE + 2 * min(s, na);             // first row of the strip (even)
         const int ss = s > 0 ? s - 1 : Gs - 1, sn = s + 1 < Gs ? s + 1 : 0;   // periodic neighbours (rows below / above)
-        const int rS = (r0 - 1 + nyu) % nyu, rN = (r0 + H) % nyu;
+        const int f = (g * HH) & 1;                         // column swap of this thread (upper group, HH odd)
+        const int c0 = 2 * t;
 
         double* ubuf = sm + OFF_U;
+        double* ub = ubuf + (size_t)(1 + g * HH) * NXU;      // the thread's local row 0 (rows -1 and HH exist too)
         double* bs = sm + OFF_B;
         double* accs = sm + OFF_A;
-        double* wedgeW = sm + OFF_E;                         // [HM][NW] W products for lane 0 of warp w + 1
-        double* wedgeE = wedgeW + (size_t)HM * NW;           // [HM][NW] E products for lane 31 of warp w - 1
+        double* wedge = sm + OFF_E + (size_t)g * 2 * HHM * NW;   // this group's [2 kinds][HHM][NW]
+        double* gx0 = sm + OFF_G;                            // per colour: [0][t] lower group's top row -> upper, [1][t] upper's bottom row -> lower
         double* red_s = sm + OFF_R;
         __shared__ int s_dec[2];
         __shared__ int s_last;
         __shared__ volatile int s_pf;                        // level whose U_k rows set p-1 has published (thread 0)
         __shared__ long long s_tr[PS_TR];
+        __shared__ long long s_tm[2];
 
+        // LL cells of a strip: [ring][side][t]; side 0 = its bottom row (published by the lower group), 1 = its top row
         unsigned long long* myx = S.llx + ((size_t)(p * Gs + s) * PS_RX * 2 * T) * 2;
-        const unsigned long long* sx = S.llx + ((size_t)(p * Gs + ss) * PS_RX * 2 * T) * 2;
-        const unsigned long long* nxq = S.llx + ((size_t)(p * Gs + sn) * PS_RX * 2 * T) * 2;
+        const unsigned long long* nbx = S.llx + ((size_t)(p * Gs + (g ? sn : ss)) * PS_RX * 2 * T) * 2;
+        auto mycell = [&](unsigned q) { return myx + ((size_t)((q % PS_RX) * 2 + g) * T + t) * 2; };
+        auto nbcell = [&](unsigned q) { return nbx + ((size_t)((q % PS_RX) * 2 + (1 - g)) * T + t) * 2; };
 
-        const int t = tid, c0 = 2 * t;
         const double omega = __ldcg(S.ctl);
         const int SW = (int)__ldcg(S.ctl + 1);
         const int chk = max(1, (int)__ldcg(S.ctl + 3));
-#define ax (S.ax)
 #define bx (S.bx)
 #define ay (S.ay)
 #define by (S.by)
 #define aC1 (S.aC1)
 #define tau (S.P.dt)
+        const double a1 = f ? -S.ax : S.ax;                  // ax seen through the column swap
+        const double sx2 = f ? -P.i2hx : P.i2hx;             // 1/(2 hx) seen through the column swap (residual)
         const double oic = omega * S.invC1, om1 = 1.0 - omega;     // x <- om1 x + oic (b - offdiag x)
-        const int wp = (w + NW - 1) % NW, wn = (w + 1) % NW;
-        const int cW = (c0 + NXU - 1) & (NXU - 1), cE = (c0 + 2) & (NXU - 1);
+        // kind A rows (other colour in local column 1): the product travels to thread t + 1 (f = 0) or t - 1 (f = 1);
+        // kind B rows (other colour in local column 0): the opposite way.
+        const int srcA = (lane + (f ? 1 : 31)) & 31, srcB = (lane + (f ? 31 : 1)) & 31;
+        const int edgeA = f ? 31 : 0, edgeB = f ? 0 : 31;    // lanes whose source lies in the neighbouring warp
+        const int wsA = f ? (wl + 1) % NW : (wl + NW - 1) % NW, wsB = f ? (wl + NW - 1) % NW : (wl + 1) % NW;
+        double* wdA = wedge;                                 // [HHM][NW]
+        double* wdB = wedge + (size_t)HHM * NW;
+        const int uo0 = c0 + f, uo1 = c0 + 1 - f;            // actual columns of local columns 0 and 1
+        const int co0 = f ? ((c0 + 2) & (NXU - 1)) : ((c0 + NXU - 1) & (NXU - 1));   // out-of-thread x-neighbour of local column 0
+        const int co1 = f ? ((c0 + NXU - 1) & (NXU - 1)) : ((c0 + 2) & (NXU - 1));   // ... of local column 1
 
         auto cbar = [&]() { __syncthreads(); };
-        auto bsm = [&](int r, int j) -> double& { return bs[(size_t)(r * 2 + j) * T + t]; };
-        auto ac = [&](int j) -> double& { return accs[(size_t)j * T + t]; };
-        auto xcell = [&](auto* base, unsigned q, int side) { return base + ((size_t)((q % PS_RX) * 2 + side) * T + t) * 2; };
+        auto bsm = [&](int r, int j) -> double& { return bs[(size_t)(r * 2 + j) * NTH + tid]; };
+        auto ac = [&](int j) -> double& { return accs[(size_t)j * NTH + tid]; };
+        auto lswap = [&](double2 v) { return f ? make_double2(v.y, v.x) : v; };   // actual <-> local column order
 
-        double x[H][2];
+        double x[HH][2];
         #pragma unroll
-        for (int j = 0; j < NB_NP; ++j) accs[(size_t)j * T + tid] = 0.0;
+        for (int j = 0; j < NB_NP; ++j) ac(j) = 0.0;
         int lastx = -1;
         unsigned qx = 0;
         int levels = 0;
         if (tid == 0) s_pf = 0;
-        const bool trace = S.trace != nullptr && t == 0;     // cycle accounts of thread 0, kept in shared memory
-        if (trace) for (int i = 0; i < PS_TR; ++i) s_tr[i] = 0;
-        __shared__ long long s_tm[2];
-        if (trace) s_tm[0] = s_tm[1] = clock64();
+        const bool trace = S.trace != nullptr && tid == 0;   // cycle accounts of thread 0, kept in shared memory
+        if (trace) {
+            for (int i = 0; i < PS_TR; ++i) s_tr[i] = 0;
+            s_tm[0] = s_tm[1] = clock64();
+        }
         auto mark = [&](int i) { if (trace) { const long long now = clock64(); s_tr[i] += now - s_tm[1]; s_tm[1] = now; } };
-        auto take = [&](const unsigned long long* q, LLc cl, unsigned f) -> double {
+        auto take = [&](const unsigned long long* q, LLc cl, unsigned fl) -> double {
             if (trace) {
                 long long a = 0;
-                const double v = ll_take_t(q, cl, f, a);
+                const double v = ll_take_t(q, cl, fl, a);
                 s_tr[3] += a;
                 return v;
             }
-            return ll_take(q, cl, f);
+            return ll_take(q, cl, fl);
         };
 
-        // ---- thread 0's side jobs (no warp is set aside for them: a ninth warp would cap registers at 168) ----
+        // ---- thread 0's side jobs (no warp is set aside for them) ----
         const unsigned* fprev = p > 0 ? S.lvl + (size_t)(p - 1) * Gs : nullptr;   // set p-1's level counters
         unsigned* fmine = S.lvl + (size_t)p * Gs + s;
         int flag_lv = 0;        // thread 0: level whose U_{k+1} rows are written but not yet published (0 = none)
@@ -145,56 +168,71 @@ struct PsEngine {
             }
         };
 
-        // tt[q] = b - (off-diagonal part of A_n) x at the colour-cc point of every row q (column j_q = (q + cc) & 1).
-        // Every point of the other colour (q, 1 - j_q) is turned into its products with the coefficients its four
-        // neighbours apply to it: a_E = ax u - bx (seen from its W neighbour), a_W = -ax u - bx, a_N = ay u - by (seen
-        // from the row below), a_S = -ay u - by.  The product for the neighbouring THREAD travels by warp shuffle (warp
-        // edges through shared memory); the neighbouring strips' rows arrive in LL cells.
-        auto gather = [&](const int cc, double (&tt)[H], const bool svc, const unsigned fbase) {
-            LLc hs, hn;
+        // tt[q] = b - (off-diagonal part of A_n) x at the colour-cc point of every own row q (local column (q + cc) & 1).
+        // Every point of the other colour is turned into its products with the coefficients its four neighbours apply
+        // to it: a_E = ax u - bx (seen from its W neighbour), a_W = -ax u - bx, a_N = ay u - by (seen from the row
+        // below), a_S = -ay u - by.  The product for the neighbouring THREAD travels by warp shuffle (warp edges through
+        // shared memory), the one for the other row group through shared memory, and the neighbouring strip's row
+        // arrives in an LL cell.
+        auto gather = [&](const int cc, double (&tt)[HH], const bool svc, const unsigned fbase) {
+            LLc hc;
             const unsigned qn = (unsigned)lastx;
-            if (lastx >= 0) {
-                hs = ll_issue(xcell(sx, qn, 1));
-                hn = ll_issue(xcell(nxq, qn, 0));
-            }
-            if (svc && t == 0 && (flag_lv | pf_lv)) service(fbase);
-            double oq[H];
+            if (lastx >= 0) hc = ll_issue(nbcell(qn));
+            if (svc && tid == 0 && (flag_lv | pf_lv)) service(fbase);
+            double oq[HH];
+            double* gx = gx0 + (size_t)cc * 2 * T;           // double-buffered: a fast warp's next half-sweep writes the other half
             #pragma unroll
-            for (int q = 0; q < H; ++q) tt[q] = bsm(q, (q + cc) & 1);
+            for (int q = 0; q < HH; ++q) tt[q] = bsm(q, (q + cc) & 1);
             #pragma unroll
-            for (int q = 0; q < H; ++q) {
-                const int jn = 1 - ((q + cc) & 1);               // the other colour's column of this row
-                const double uq = ubuf[(size_t)(q + 1) * NXU + c0 + jn], xq = x[q][jn];
+            for (int q = 0; q < HH; ++q) {
+                const int jn = 1 - ((q + cc) & 1);               // the other colour's local column in this row
+                const double uq = ub[(size_t)q * NXU + (jn ? uo1 : uo0)], xq = x[q][jn];
                 const double m = uq * xq, bxq = bx * xq, byq = by * xq;
-                const double eq = fma(ax, m, -bxq), wq = fma(-ax, m, -bxq);
-                if (jn == 1) { tt[q] -= eq; oq[q] = wq; } else { tt[q] -= wq; oq[q] = eq; }
-                if (q > 0) tt[q > 0 ? q - 1 : 0] -= fma(ay, m, -byq);
-                if (q + 1 < H) tt[q + 1 < H ? q + 1 : q] -= fma(-ay, m, -byq);
-                if (jn == 1) { if (lane == 31) wedgeW[q * NW + w] = wq; }
-                else { if (lane == 0) wedgeE[q * NW + w] = eq; }
+                const double pa = fma(a1, m, -bxq), pb = fma(-a1, m, -bxq);
+                const double pn = fma(ay, m, -byq), psv = fma(-ay, m, -byq);
+                if (jn == 1) {               // kind A: in-thread term pa, travelling term pb
+                    tt[q] -= pa; oq[q] = pb;
+                    if (lane == 31 - edgeA) wdA[q * NW + wl] = pb;
+                } else {                     // kind B: in-thread term pb, travelling term pa
+                    tt[q] -= pb; oq[q] = pa;
+                    if (lane == 31 - edgeB) wdB[q * NW + wl] = pa;
+                }
+                if (q > 0) tt[q > 0 ? q - 1 : 0] -= pn;
+                else if (g == 1) gx[T + t] = pn;             // to the lower group's top row
+                if (q + 1 < HH) tt[q + 1 < HH ? q + 1 : q] -= psv;
+                else if (g == 0) gx[t] = psv;                // to the upper group's bottom row
             }
             cbar();
             #pragma unroll
-            for (int q = 0; q < H; ++q) {
+            for (int q = 0; q < HH; ++q) {
                 const int jn = 1 - ((q + cc) & 1);
                 double in;
-                if (jn == 1) {       // active column 0: W neighbour = thread t-1's column 1
-                    in = __shfl_up_sync(0xffffffffu, oq[q], 1);
-                    const double e = wedgeW[q * NW + wp];
-                    in = lane == 0 ? e : in;
-                } else {             // active column 1: E neighbour = thread t+1's column 0
-                    in = __shfl_down_sync(0xffffffffu, oq[q], 1);
-                    const double e = wedgeE[q * NW + wn];
-                    in = lane == 31 ? e : in;
+                if (jn == 1) {
+                    in = __shfl_sync(0xffffffffu, oq[q], srcA);
+                    const double e = wdA[q * NW + wsA];
+                    in = lane == edgeA ? e : in;
+                } else {
+                    in = __shfl_sync(0xffffffffu, oq[q], srcB);
+                    const double e = wdB[q * NW + wsB];
+                    in = lane == edgeB ? e : in;
                 }
                 tt[q] -= in;
             }
-            if (lastx >= 0) {        // the neighbouring strips' boundary rows (their last publication: the other colour)
-                const double xs_h = take(xcell(sx, qn, 1), hs, qn + 1u);
-                const double xn_h = take(xcell(nxq, qn, 0), hn, qn + 1u);
-                const double uS = ubuf[c0 + (cc & 1)], uN = ubuf[(size_t)(H + 1) * NXU + c0 + ((H - 1 + cc) & 1)];
-                tt[0] = fma(-fma(-ay, uS, -by), xs_h, tt[0]);
-                tt[H - 1] = fma(-fma(ay, uN, -by), xn_h, tt[H - 1]);
+            // the row below local row 0 and the row above local row HH-1: the other row group or the neighbouring strip
+            if (g == 0) {
+                tt[HH - 1] -= gx[T + t];
+                if (lastx >= 0) {
+                    const double xh = take(nbcell(qn), hc, qn + 1u);
+                    const double uh = ub[-(ptrdiff_t)NXU + ((cc & 1) ? uo1 : uo0)];
+                    tt[0] = fma(-fma(-ay, uh, -by), xh, tt[0]);
+                }
+            } else {
+                tt[0] -= gx[t];
+                if (lastx >= 0) {
+                    const double xh = take(nbcell(qn), hc, qn + 1u);
+                    const double uh = ub[(size_t)HH * NXU + (((HH - 1 + cc) & 1) ? uo1 : uo0)];
+                    tt[HH - 1] = fma(-fma(ay, uh, -by), xh, tt[HH - 1]);
+                }
             }
         };
 
@@ -203,22 +241,23 @@ struct PsEngine {
             const bool active = p < D && k < S.newton_max;
             const double* Uk = S.U + (size_t)(k % B) * nt * ns;
             const unsigned fbase = (unsigned)pass * (unsigned)nt;
-            double2 pf[H + 2];                                   // u^n rows r0-1 .. r0+H of the level about to start
+            const int rg0 = r0 + g * HH;                         // global row of local row 0
+            double2 pf[HH + 2];                                  // u^n local rows -1 .. HH of the level about to start (local column order)
             auto load_pf = [&](int lv) {
-                const double* un = Uk + (size_t)(lv - 1) * ns;
-                pf[0] = ldcg2(un + (size_t)rS * NXU + c0);
+                const double* un = Uk + (size_t)(lv - 1) * ns + c0;
+                pf[0] = lswap(ldcg2(un + (size_t)((rg0 - 1 + nyu) % nyu) * NXU));
                 #pragma unroll
-                for (int r = 0; r < H; ++r) pf[r + 1] = ldcg2(un + (size_t)(r0 + r) * NXU + c0);
-                pf[H + 1] = ldcg2(un + (size_t)rN * NXU + c0);
+                for (int r = 0; r < HH; ++r) pf[r + 1] = lswap(ldcg2(un + (size_t)(rg0 + r) * NXU));
+                pf[HH + 1] = lswap(ldcg2(un + (size_t)((rg0 + HH) % nyu) * NXU));
             };
             if (active) {
                 #pragma unroll
-                for (int r = 0; r < H; ++r) {
+                for (int r = 0; r < HH; ++r) {
                     x[r][0] = 0.0; x[r][1] = 0.0;
-                    *reinterpret_cast<double2*>(ubuf + (size_t)(r + 1) * NXU + c0) = ldcg2(S.u0 + (size_t)(r0 + r) * NXU + c0);   // u^{n-1} of level 1
+                    *reinterpret_cast<double2*>(ub + (size_t)r * NXU + c0) = ldcg2(S.u0 + (size_t)(rg0 + r) * NXU + c0);   // u^{n-1} of level 1
                 }
                 lastx = -1;
-                if (t == 0) {
+                if (tid == 0) {
                     pf_lv = 1;
                     for (;;) {
                         service(fbase);
@@ -234,30 +273,30 @@ struct PsEngine {
                 mark(6);
                 // ---- prologue 1: b = du^{n-1} - (u^n - u^{n-1}); u^n replaces u^{n-1} in shared memory
                 #pragma unroll
-                for (int r = 0; r < H; ++r) {
-                    double2* up = reinterpret_cast<double2*>(ubuf + (size_t)(r + 1) * NXU + c0);
-                    const double2 old = *up;
+                for (int r = 0; r < HH; ++r) {
+                    double2* up = reinterpret_cast<double2*>(ub + (size_t)r * NXU + c0);
+                    const double2 old = lswap(*up);
                     bsm(r, 0) = x[r][0] - (pf[r + 1].x - old.x);
                     bsm(r, 1) = x[r][1] - (pf[r + 1].y - old.y);
-                    *up = pf[r + 1];
+                    *up = lswap(pf[r + 1]);
                 }
-                *reinterpret_cast<double2*>(ubuf + c0) = pf[0];
-                *reinterpret_cast<double2*>(ubuf + (size_t)(H + 1) * NXU + c0) = pf[H + 1];
+                if (g == 0) *reinterpret_cast<double2*>(ub - (ptrdiff_t)NXU + c0) = lswap(pf[0]);
+                else *reinterpret_cast<double2*>(ub + (size_t)HH * NXU + c0) = lswap(pf[HH + 1]);
                 cbar();
-                if (t == 0 && n < nt) pf_lv = n + 1;
+                if (tid == 0 && n < nt) pf_lv = n + 1;
                 mark(0);
-                // ---- prologue 2: r^n = -G^n, b = r^n + du^{n-1}
+                // ---- prologue 2: r^n = -G^n, b = r^n + du^{n-1} (local column order: the x-differences carry sx2)
                 {
                     double ar2 = 0.0, arm = 0.0;
                     #pragma unroll
-                    for (int r = 0; r < H; ++r) {
+                    for (int r = 0; r < HH; ++r) {
                         const double2 prv = pf[r], cur = pf[r + 1], nxt = pf[r + 2];
-                        const double uw = ubuf[(size_t)(r + 1) * NXU + cW], ue = ubuf[(size_t)(r + 1) * NXU + cE];
-                        // column 0: W = uw, E = cur.y; column 1: W = cur.x, E = ue
-                        const double conv0 = 0.5 * ((cur.y * cur.y - uw * uw) * P.i2hx + (nxt.x * nxt.x - prv.x * prv.x) * P.i2hy);
-                        const double visc0 = P.m0 * ((cur.y - 2.0 * cur.x + uw) * P.ihx2 + (nxt.x - 2.0 * cur.x + prv.x) * P.ihy2);
-                        const double conv1 = 0.5 * ((ue * ue - cur.x * cur.x) * P.i2hx + (nxt.y * nxt.y - prv.y * prv.y) * P.i2hy);
-                        const double visc1 = P.m0 * ((ue - 2.0 * cur.y + cur.x) * P.ihx2 + (nxt.y - 2.0 * cur.y + prv.y) * P.ihy2);
+                        const double o0 = ub[(size_t)r * NXU + co0], o1 = ub[(size_t)r * NXU + co1];
+                        // local column 0: x-neighbours o0 (outside) and cur.y; local column 1: cur.x and o1 (outside)
+                        const double conv0 = 0.5 * ((cur.y * cur.y - o0 * o0) * sx2 + (nxt.x * nxt.x - prv.x * prv.x) * P.i2hy);
+                        const double visc0 = P.m0 * ((cur.y - 2.0 * cur.x + o0) * P.ihx2 + (nxt.x - 2.0 * cur.x + prv.x) * P.ihy2);
+                        const double conv1 = 0.5 * ((o1 * o1 - cur.x * cur.x) * sx2 + (nxt.y * nxt.y - prv.y * prv.y) * P.i2hy);
+                        const double visc1 = P.m0 * ((o1 - 2.0 * cur.y + cur.x) * P.ihx2 + (nxt.y - 2.0 * cur.y + prv.y) * P.ihy2);
                         const double f0 = tau * (conv0 - visc0), f1 = tau * (conv1 - visc1);
                         const double b0 = bsm(r, 0), b1 = bsm(r, 1);
                         const double G0 = (x[r][0] - b0) + f0, G1 = (x[r][1] - b1) + f1;     // (u^n - u^{n-1}) + tau F(u^n)
@@ -276,25 +315,25 @@ struct PsEngine {
                     const bool lastm = m == SW - 1 && chkl;
                     #pragma unroll
                     for (int cc = 0; cc < 2; ++cc) {
-                        double tt[H];
+                        double tt[HH];
                         gather(cc, tt, true, fbase);
                         double rs2 = 0.0, rsm = 0.0;
                         #pragma unroll
-                        for (int i = 0; i < H; ++i) {
-                            const int r = i == 0 ? 0 : (i == 1 ? H - 1 : i - 1);     // boundary rows first
-                            const int j = (r + cc) & 1;
-                            const double xo = x[r][j];
-                            const double xn = fma(oic, tt[r], om1 * xo);
-                            x[r][j] = xn;
-                            if (cc == 1 && lastm) {
-                                const double rr = aC1 * (om1 / omega) * (xn - xo);
-                                rs2 = fma(rr, rr, rs2);
-                                rsm = fmax(rsm, fabs(rr));
-                            }
-                            if (i == (H > 1 ? 1 : 0)) {
-                                const unsigned f = qx + 1u;
-                                ll_put(xcell(myx, qx, 0), x[0][cc & 1], f);
-                                ll_put(xcell(myx, qx, 1), x[H - 1][(H - 1 + cc) & 1], f);
+                        for (int i = 0; i < HH; ++i) {
+                            // the strip's boundary row first (local row 0 of the lower group, HH-1 of the upper group)
+                            const int rl = i, ru = HH - 1 - i;
+                            if (g == 0) {
+                                const int j = (rl + cc) & 1;
+                                const double xo = x[rl][j], xn = fma(oic, tt[rl], om1 * xo);
+                                x[rl][j] = xn;
+                                if (cc == 1 && lastm) { const double rr = aC1 * (om1 / omega) * (xn - xo); rs2 = fma(rr, rr, rs2); rsm = fmax(rsm, fabs(rr)); }
+                                if (i == 0) ll_put(mycell(qx), xn, qx + 1u);
+                            } else {
+                                const int j = (ru + cc) & 1;
+                                const double xo = x[ru][j], xn = fma(oic, tt[ru], om1 * xo);
+                                x[ru][j] = xn;
+                                if (cc == 1 && lastm) { const double rr = aC1 * (om1 / omega) * (xn - xo); rs2 = fma(rr, rr, rs2); rsm = fmax(rsm, fabs(rr)); }
+                                if (i == 0) ll_put(mycell(qx), xn, qx + 1u);
                             }
                         }
                         if (cc == 1 && lastm) {
@@ -315,26 +354,26 @@ struct PsEngine {
                     double* Un = S.U + (size_t)((k + 1) % B) * nt * ns + (size_t)(n - 1) * ns;
                     double d2 = 0.0, dm = 0.0;
                     #pragma unroll
-                    for (int r = 0; r < H; ++r) {
-                        double2 v = *reinterpret_cast<const double2*>(ubuf + (size_t)(r + 1) * NXU + c0);
+                    for (int r = 0; r < HH; ++r) {
+                        double2 v = lswap(*reinterpret_cast<const double2*>(ub + (size_t)r * NXU + c0));
                         v.x += x[r][0];
                         v.y += x[r][1];
-                        *reinterpret_cast<double2*>(Un + (size_t)(r0 + r) * NXU + c0) = v;
+                        *reinterpret_cast<double2*>(Un + (size_t)(rg0 + r) * NXU + c0) = lswap(v);
                         d2 = fma(x[r][0], x[r][0], fma(x[r][1], x[r][1], d2));
                         dm = fmax(dm, fmax(fabs(x[r][0]), fabs(x[r][1])));
                     }
                     ac(2) += d2;
                     ac(3) = fmax(ac(3), dm);
-                    if (t == 0) flag_lv = n;                        // published by service() after the next CTA barrier
+                    if (tid == 0) flag_lv = n;                      // published by service() after the next CTA barrier
                 }
                 mark(4);
                 // ---- a-posteriori residual of the red points after the final black half-sweep
                 if (chkl) {
-                    double tt[H];
+                    double tt[HH];
                     gather(0, tt, false, fbase);
                     double rs2 = 0.0, rsm = 0.0, bb2 = 0.0;
                     #pragma unroll
-                    for (int r = 0; r < H; ++r) {
+                    for (int r = 0; r < HH; ++r) {
                         const double rr = tt[r] - aC1 * x[r][r & 1];
                         rs2 = fma(rr, rr, rs2);
                         rsm = fmax(rsm, fabs(rr));
@@ -364,22 +403,22 @@ struct PsEngine {
                         #pragma unroll
                         for (int j = 0; j < NB_NP; ++j) red_s[w * NB_NP + j] = a[j];
                     cbar();
-                    if (t == 0) {
+                    if (tid == 0) {
                         service(fbase);                            // level nt's counter (fence inside)
                         double* hp = S.hpart + ((size_t)k * Gs + s) * NB_NP;
                         for (int j = 0; j < NB_NP; ++j) {
                             double v = red_s[j];
-                            for (int ww = 1; ww < NW; ++ww) v = nb_is_max(j) ? fmax(v, red_s[ww * NB_NP + j]) : v + red_s[ww * NB_NP + j];
+                            for (int ww = 1; ww < 2 * NW; ++ww) v = nb_is_max(j) ? fmax(v, red_s[ww * NB_NP + j]) : v + red_s[ww * NB_NP + j];
                             hp[j] = v;
                         }
                         __threadfence();
                         s_last = atomicAdd(S.arrive + k, 1u) == (unsigned)(Gs - 1);
                     }
                     cbar();
-                    if (s_last && t < 32) {
+                    if (s_last && tid < 32) {
                         __threadfence();
                         double g4[NB_NP] = {0, 0, 0, 0, 0, 0, 0};
-                        for (int gg = t; gg < Gs; gg += 32) {
+                        for (int gg = tid; gg < Gs; gg += 32) {
                             const double* hp = S.hpart + ((size_t)k * Gs + gg) * NB_NP;
                             #pragma unroll
                             for (int j = 0; j < NB_NP; ++j) {
@@ -394,7 +433,7 @@ struct PsEngine {
                                 const double y = __shfl_xor_sync(0xffffffffu, g4[j], o);
                                 g4[j] = nb_is_max(j) ? fmax(g4[j], y) : g4[j] + y;
                             }
-                        if (t == 0) {
+                        if (tid == 0) {
                             const double Ntot = (double)ns * (double)nt;
                             S.hist[4 * k + 0] = sqrt(g4[0] / Ntot);
                             S.hist[4 * k + 1] = g4[1];
@@ -424,10 +463,12 @@ struct PsEngine {
                         }
                     }
                 }
-                // ---- (rare) set p-1 had not published the next level yet: wait for it, then load
-                if (!pf_loaded && s_pf == n + 1) { load_pf(n + 1); pf_loaded = true; }
-                while (!pf_loaded) {
-                    if (t == 0) {
+                // ---- the next level's u rows if they are not loaded yet (levels with a residual check, or set p-1 had not
+                //      published them): thread 0 waits for set p-1's counters.  pf_loaded is CTA-uniform: s_pf was read
+                //      right behind a barrier, and thread 0 calls service() again only behind the next one.
+                if (!pf_loaded) {
+                    cbar();                                         // every thread's U_{k+1}^n rows are stored: service() may publish them
+                    if (tid == 0) {
                         for (;;) {
                             service(fbase);
                             if (!pf_lv) break;
@@ -435,7 +476,7 @@ struct PsEngine {
                         }
                     }
                     cbar();
-                    if (s_pf == n + 1) { load_pf(n + 1); pf_loaded = true; }
+                    load_pf(n + 1);
                 }
                 cbar();                                             // every thread is done reading this level's u
             }
@@ -478,7 +519,6 @@ struct PsEngine {
             }
         }
         copy_out(S, s_dec[1]);
-#undef ax
 #undef bx
 #undef ay
 #undef by
@@ -503,13 +543,13 @@ struct PsEngine {
 };
 
 template <int NXU, int HE>
-__global__ void __launch_bounds__(NXU / 2, 1) k_newton_ps(const PsParams S) {
+__global__ void __launch_bounds__(NXU, 1) k_newton_ps(const PsParams S) {
     extern __shared__ __align__(128) double sm_ps[];
     using E = PsEngine<NXU, HE>;
     if ((int)blockIdx.x >= S.D * S.Gs) return;
     const int s = blockIdx.x % S.Gs;
     const int na = (S.P.nyu - HE * S.Gs) / 2;
-    if (s < na) E::template run<HE + 2>(S, sm_ps); else E::template run<HE>(S, sm_ps);
+    if (s < na) E::template run<HE / 2 + 1>(S, sm_ps); else E::template run<HE / 2>(S, sm_ps);
 }
 
 }  // namespace pit
