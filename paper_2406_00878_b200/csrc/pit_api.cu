@@ -105,6 +105,7 @@ struct pit_handle {
         int x0carry = 1;          // PIT_X0=0: engines 2-3 start level solves from 0 instead of the carry
         bool merge = true;        // PIT_MERGE=0: engine 3 without the merged first BiCGSTAB iteration
         bool guess_graph = true;  // PIT_GUESS_GRAPH=0: the coarse-grid march without a CUDA graph
+        int ps_dbg = 0;           // PIT_PS_DBG: engine-5 timing experiments (bit 0: no LL waits — wrong results)
     } dbg;
     int c_march_ring = -1;        // the ring presence the coarse-march graph was captured with (-1: none captured)
     // caller-owned workspace (pit_create_with_workspace): every create-time buffer is carved from it
@@ -365,6 +366,7 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
         h->dbg.x0carry = env_int("PIT_X0", 1);
         h->dbg.merge = env_int("PIT_MERGE", 1) != 0;
         h->dbg.guess_graph = env_int("PIT_GUESS_GRAPH", 1) != 0;
+        h->dbg.ps_dbg = env_int("PIT_PS_DBG", 0);
     }
     pit_config& c = h->cfg;
     if (c.lin_rtol == 0.0) c.lin_rtol = 1e-6;     // inexact-Newton forcing term (R10)
@@ -779,6 +781,7 @@ static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double*
     S.trace = h->trace ? h->trace + 13 + 13 * GMAX2 : nullptr;
     S.ax = P.dt * P.i2hx; S.bx = P.dt * P.m0 * P.ihx2; S.ay = P.dt * P.i2hy; S.by = P.dt * P.m0 * P.ihy2;
     S.aC1 = 1.0 + 2.0 * (S.bx + S.by); S.invC1 = 1.0 / S.aC1;
+    S.dbg = h->dbg.ps_dbg;
     void* args[] = {(void*)&S};
     size_t smem5 = 0;
     int thr5 = 0;

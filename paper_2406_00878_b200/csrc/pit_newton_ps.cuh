@@ -34,6 +34,13 @@ __device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
+    unsigned ok;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+    } while (!ok);
+}
 __device__ __forceinline__ unsigned ld_rlx(const unsigned* p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -85,7 +92,6 @@ struct PsEngine {
         double* red_s = sm + OFF_R;
         __shared__ int s_dec[2];
         __shared__ int s_last;
-        __shared__ volatile int s_pf;                        // level whose U_k rows set p-1 has published (thread 0)
         __shared__ long long s_tr[PS_TR];
         __shared__ long long s_tm[2];
 
@@ -113,9 +119,13 @@ struct PsEngine {
         const int wsA = f ? (wl + 1) % NW : (wl + NW - 1) % NW, wsB = f ? (wl + NW - 1) % NW : (wl + 1) % NW;
         double* wdA = wedge;                                 // [HHM][NW]
         double* wdB = wedge + (size_t)HHM * NW;
-        const int uo0 = c0 + f, uo1 = c0 + 1 - f;            // actual columns of local columns 0 and 1
-        const int co0 = f ? ((c0 + 2) & (NXU - 1)) : ((c0 + NXU - 1) & (NXU - 1));   // out-of-thread x-neighbour of local column 0
-        const int co1 = f ? ((c0 + NXU - 1) & (NXU - 1)) : ((c0 + 2) & (NXU - 1));   // ... of local column 1
+        const int isA = lane == edgeA, isB = lane == edgeB;
+        // ubuf rows are de-interleaved: [even columns (T)][odd columns (T)], so that a warp's loads of one local column
+        // are contiguous (no bank conflicts).  Offsets of local columns 0 and 1, and of their out-of-thread x-neighbours
+        // (actual column c0 - 1: odd, pair t - 1; actual column c0 + 2: even, pair t + 1; periodic).
+        const int uo0 = f * T + t, uo1 = (1 - f) * T + t;
+        const int cwest = T + (t + T - 1) % T, ceast = (t + 1) % T;
+        const int co0 = f ? ceast : cwest, co1 = f ? cwest : ceast;
 
         auto cbar = [&]() { __syncthreads(); };
         auto bsm = [&](int r, int j) -> double& { return bs[(size_t)(r * 2 + j) * NTH + tid]; };
@@ -128,7 +138,6 @@ struct PsEngine {
         int lastx = -1;
         unsigned qx = 0;
         int levels = 0;
-        if (tid == 0) s_pf = 0;
         const bool trace = S.trace != nullptr && tid == 0;   // cycle accounts of thread 0, kept in shared memory
         if (trace) {
             for (int i = 0; i < PS_TR; ++i) s_tr[i] = 0;
@@ -136,6 +145,7 @@ struct PsEngine {
         }
         auto mark = [&](int i) { if (trace) { const long long now = clock64(); s_tr[i] += now - s_tm[1]; s_tm[1] = now; } };
         auto take = [&](const unsigned long long* q, LLc cl, unsigned fl) -> double {
+            if (S.dbg & 1) return __hiloint2double((int)(unsigned)cl.w1, (int)(unsigned)cl.w0);   // timing experiment: no wait
             if (trace) {
                 long long a = 0;
                 const double v = ll_take_t(q, cl, fl, a);
@@ -162,10 +172,7 @@ struct PsEngine {
                 asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(fmine), "r"(base + (unsigned)flag_lv) : "memory");
                 flag_lv = 0;
             }
-            if (ready) {
-                s_pf = pf_lv;
-                pf_lv = 0;
-            }
+            if (ready) pf_lv = 0;
         };
 
         // tt[q] = b - (off-diagonal part of A_n) x at the colour-cc point of every own row q (local column (q + cc) & 1).
@@ -179,7 +186,6 @@ struct PsEngine {
             const unsigned qn = (unsigned)lastx;
             if (lastx >= 0) hc = ll_issue(nbcell(qn));
             if (svc && tid == 0 && (flag_lv | pf_lv)) service(fbase);
-            double oq[HH];
             double* gx = gx0 + (size_t)cc * 2 * T;           // double-buffered: a fast warp's next half-sweep writes the other half
             #pragma unroll
             for (int q = 0; q < HH; ++q) tt[q] = bsm(q, (q + cc) & 1);
@@ -190,11 +196,17 @@ struct PsEngine {
                 const double m = uq * xq, bxq = bx * xq, byq = by * xq;
                 const double pa = fma(a1, m, -bxq), pb = fma(-a1, m, -bxq);
                 const double pn = fma(ay, m, -byq), psv = fma(-ay, m, -byq);
+                // the travelling product goes to the neighbouring thread at once (shuffle); the lanes whose source lies in
+                // the neighbouring warp take theirs from shared memory behind the barrier instead
                 if (jn == 1) {               // kind A: in-thread term pa, travelling term pb
-                    tt[q] -= pa; oq[q] = pb;
+                    const double in = __shfl_sync(0xffffffffu, pb, srcA);
+                    tt[q] -= pa;
+                    if (!isA) tt[q] -= in;
                     if (lane == 31 - edgeA) wdA[q * NW + wl] = pb;
                 } else {                     // kind B: in-thread term pb, travelling term pa
-                    tt[q] -= pb; oq[q] = pa;
+                    const double in = __shfl_sync(0xffffffffu, pa, srcB);
+                    tt[q] -= pb;
+                    if (!isB) tt[q] -= in;
                     if (lane == 31 - edgeB) wdB[q * NW + wl] = pa;
                 }
                 if (q > 0) tt[q > 0 ? q - 1 : 0] -= pn;
@@ -203,20 +215,15 @@ struct PsEngine {
                 else if (g == 0) gx[t] = psv;                // to the upper group's bottom row
             }
             cbar();
-            #pragma unroll
-            for (int q = 0; q < HH; ++q) {
-                const int jn = 1 - ((q + cc) & 1);
-                double in;
-                if (jn == 1) {
-                    in = __shfl_sync(0xffffffffu, oq[q], srcA);
-                    const double e = wdA[q * NW + wsA];
-                    in = lane == edgeA ? e : in;
-                } else {
-                    in = __shfl_sync(0xffffffffu, oq[q], srcB);
-                    const double e = wdB[q * NW + wsB];
-                    in = lane == edgeB ? e : in;
-                }
-                tt[q] -= in;
+            if (isA) {
+                #pragma unroll
+                for (int q = 0; q < HH; ++q)
+                    if ((q + cc) & 1) {} else tt[q] -= wdA[q * NW + wsA];      // kind A rows: other colour in local column 1
+            }
+            if (isB) {
+                #pragma unroll
+                for (int q = 0; q < HH; ++q)
+                    if ((q + cc) & 1) tt[q] -= wdB[q * NW + wsB];              // kind B rows
             }
             // the row below local row 0 and the row above local row HH-1: the other row group or the neighbouring strip
             if (g == 0) {
@@ -242,61 +249,65 @@ struct PsEngine {
             const double* Uk = S.U + (size_t)(k % B) * nt * ns;
             const unsigned fbase = (unsigned)pass * (unsigned)nt;
             const int rg0 = r0 + g * HH;                         // global row of local row 0
-            double2 pf[HH + 2];                                  // u^n local rows -1 .. HH of the level about to start (local column order)
-            auto load_pf = [&](int lv) {
-                const double* un = Uk + (size_t)(lv - 1) * ns + c0;
-                pf[0] = lswap(ldcg2(un + (size_t)((rg0 - 1 + nyu) % nyu) * NXU));
-                #pragma unroll
-                for (int r = 0; r < HH; ++r) pf[r + 1] = lswap(ldcg2(un + (size_t)(rg0 + r) * NXU));
-                pf[HH + 1] = lswap(ldcg2(un + (size_t)((rg0 + HH) % nyu) * NXU));
-            };
             if (active) {
                 #pragma unroll
                 for (int r = 0; r < HH; ++r) {
                     x[r][0] = 0.0; x[r][1] = 0.0;
-                    *reinterpret_cast<double2*>(ub + (size_t)r * NXU + c0) = ldcg2(S.u0 + (size_t)(rg0 + r) * NXU + c0);   // u^{n-1} of level 1
+                    const double2 v = ldcg2(S.u0 + (size_t)(rg0 + r) * NXU + c0);     // u^{n-1} of level 1
+                    ub[(size_t)r * NXU + t] = v.x;
+                    ub[(size_t)r * NXU + T + t] = v.y;
                 }
                 lastx = -1;
-                if (tid == 0) {
-                    pf_lv = 1;
-                    for (;;) {
-                        service(fbase);
-                        if (!pf_lv) break;
-                        __nanosleep(64);
-                    }
-                }
-                cbar();
-                load_pf(1);
+                if (tid == 0) pf_lv = 1;
             }
             for (int n = 1; active && n <= nt; ++n) {
                 ++levels;
                 mark(6);
-                // ---- prologue 1: b = du^{n-1} - (u^n - u^{n-1}); u^n replaces u^{n-1} in shared memory
-                #pragma unroll
-                for (int r = 0; r < HH; ++r) {
-                    double2* up = reinterpret_cast<double2*>(ub + (size_t)r * NXU + c0);
-                    const double2 old = lswap(*up);
-                    bsm(r, 0) = x[r][0] - (pf[r + 1].x - old.x);
-                    bsm(r, 1) = x[r][1] - (pf[r + 1].y - old.y);
-                    *up = lswap(pf[r + 1]);
+                // ---- set p-1 must have published U_k^n (normally confirmed by service() during the previous level)
+                cbar();                                             // every thread has stored level n-1 and is done reading its u
+                if (tid == 0) {
+                    while (pf_lv) {
+                        service(fbase);
+                        if (pf_lv) __nanosleep(64);
+                    }
                 }
-                if (g == 0) *reinterpret_cast<double2*>(ub - (ptrdiff_t)NXU + c0) = lswap(pf[0]);
-                else *reinterpret_cast<double2*>(ub + (size_t)HH * NXU + c0) = lswap(pf[HH + 1]);
+                cbar();
+                // ---- prologue 1: b = du^{n-1} - (u^n - u^{n-1}); u^n replaces u^{n-1} in shared memory
+                {
+                    const double* un = Uk + (size_t)(n - 1) * ns + c0;
+                    double2 pf[HH + 1];                             // own rows, then this group's strip-halo row
+                    #pragma unroll
+                    for (int r = 0; r < HH; ++r) pf[r] = ldcg2(un + (size_t)(rg0 + r) * NXU);
+                    pf[HH] = ldcg2(un + (size_t)(g ? (rg0 + HH) % nyu : (rg0 - 1 + nyu) % nyu) * NXU);
+                    #pragma unroll
+                    for (int r = 0; r < HH; ++r) {
+                        const double2 nw = lswap(pf[r]);
+                        bsm(r, 0) = x[r][0] - (nw.x - ub[(size_t)r * NXU + uo0]);
+                        bsm(r, 1) = x[r][1] - (nw.y - ub[(size_t)r * NXU + uo1]);
+                        ub[(size_t)r * NXU + t] = pf[r].x;
+                        ub[(size_t)r * NXU + T + t] = pf[r].y;
+                    }
+                    double* hrow = g ? ub + (size_t)HH * NXU : ub - (ptrdiff_t)NXU;
+                    hrow[t] = pf[HH].x;
+                    hrow[T + t] = pf[HH].y;
+                }
                 cbar();
                 if (tid == 0 && n < nt) pf_lv = n + 1;
                 mark(0);
                 // ---- prologue 2: r^n = -G^n, b = r^n + du^{n-1} (local column order: the x-differences carry sx2)
                 {
                     double ar2 = 0.0, arm = 0.0;
+                    double p0 = ub[-(ptrdiff_t)NXU + uo0], p1 = ub[-(ptrdiff_t)NXU + uo1];
+                    double c0v = ub[uo0], c1v = ub[uo1];
                     #pragma unroll
                     for (int r = 0; r < HH; ++r) {
-                        const double2 prv = pf[r], cur = pf[r + 1], nxt = pf[r + 2];
+                        const double n0 = ub[(size_t)(r + 1) * NXU + uo0], n1 = ub[(size_t)(r + 1) * NXU + uo1];
                         const double o0 = ub[(size_t)r * NXU + co0], o1 = ub[(size_t)r * NXU + co1];
-                        // local column 0: x-neighbours o0 (outside) and cur.y; local column 1: cur.x and o1 (outside)
-                        const double conv0 = 0.5 * ((cur.y * cur.y - o0 * o0) * sx2 + (nxt.x * nxt.x - prv.x * prv.x) * P.i2hy);
-                        const double visc0 = P.m0 * ((cur.y - 2.0 * cur.x + o0) * P.ihx2 + (nxt.x - 2.0 * cur.x + prv.x) * P.ihy2);
-                        const double conv1 = 0.5 * ((o1 * o1 - cur.x * cur.x) * sx2 + (nxt.y * nxt.y - prv.y * prv.y) * P.i2hy);
-                        const double visc1 = P.m0 * ((o1 - 2.0 * cur.y + cur.x) * P.ihx2 + (nxt.y - 2.0 * cur.y + prv.y) * P.ihy2);
+                        // local column 0: x-neighbours o0 (outside) and c1v; local column 1: c0v and o1 (outside)
+                        const double conv0 = 0.5 * ((c1v * c1v - o0 * o0) * sx2 + (n0 * n0 - p0 * p0) * P.i2hy);
+                        const double visc0 = P.m0 * ((c1v - 2.0 * c0v + o0) * P.ihx2 + (n0 - 2.0 * c0v + p0) * P.ihy2);
+                        const double conv1 = 0.5 * ((o1 * o1 - c0v * c0v) * sx2 + (n1 * n1 - p1 * p1) * P.i2hy);
+                        const double visc1 = P.m0 * ((o1 - 2.0 * c1v + c0v) * P.ihx2 + (n1 - 2.0 * c1v + p1) * P.ihy2);
                         const double f0 = tau * (conv0 - visc0), f1 = tau * (conv1 - visc1);
                         const double b0 = bsm(r, 0), b1 = bsm(r, 1);
                         const double G0 = (x[r][0] - b0) + f0, G1 = (x[r][1] - b1) + f1;     // (u^n - u^{n-1}) + tau F(u^n)
@@ -304,6 +315,7 @@ struct PsEngine {
                         bsm(r, 1) = b1 - f1;
                         ar2 = fma(G0, G0, fma(G1, G1, ar2));
                         arm = fmax(arm, fmax(fabs(G0), fabs(G1)));
+                        p0 = c0v; p1 = c1v; c0v = n0; c1v = n1;
                     }
                     ac(0) += ar2;
                     ac(1) = fmax(ac(1), arm);
@@ -320,21 +332,17 @@ struct PsEngine {
                         double rs2 = 0.0, rsm = 0.0;
                         #pragma unroll
                         for (int i = 0; i < HH; ++i) {
-                            // the strip's boundary row first (local row 0 of the lower group, HH-1 of the upper group)
-                            const int rl = i, ru = HH - 1 - i;
-                            if (g == 0) {
-                                const int j = (rl + cc) & 1;
-                                const double xo = x[rl][j], xn = fma(oic, tt[rl], om1 * xo);
-                                x[rl][j] = xn;
-                                if (cc == 1 && lastm) { const double rr = aC1 * (om1 / omega) * (xn - xo); rs2 = fma(rr, rr, rs2); rsm = fmax(rsm, fabs(rr)); }
-                                if (i == 0) ll_put(mycell(qx), xn, qx + 1u);
-                            } else {
-                                const int j = (ru + cc) & 1;
-                                const double xo = x[ru][j], xn = fma(oic, tt[ru], om1 * xo);
-                                x[ru][j] = xn;
-                                if (cc == 1 && lastm) { const double rr = aC1 * (om1 / omega) * (xn - xo); rs2 = fma(rr, rr, rs2); rsm = fmax(rsm, fabs(rr)); }
-                                if (i == 0) ll_put(mycell(qx), xn, qx + 1u);
+                            const int r = i == 0 ? 0 : (i == 1 ? HH - 1 : i - 1);     // the two end rows first: one of them is the strip's boundary row
+                            const int j = (r + cc) & 1;
+                            const double xo = x[r][j], xn = fma(oic, tt[r], om1 * xo);
+                            x[r][j] = xn;
+                            if (cc == 1 && lastm) {
+                                const double rr = aC1 * (om1 / omega) * (xn - xo);
+                                rs2 = fma(rr, rr, rs2);
+                                rsm = fmax(rsm, fabs(rr));
                             }
+                            if (i == (HH > 1 ? 1 : 0))       // publish: local row 0 of the lower group, HH-1 of the upper group
+                                ll_put(mycell(qx), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
                         }
                         if (cc == 1 && lastm) {
                             ac(4) += rs2;
@@ -345,19 +353,15 @@ struct PsEngine {
                     }
                 }
                 mark(2);
-                // ---- the next level's u rows (registers), if set p-1 has published them
-                bool pf_loaded = n == nt;
-                cbar();                                             // s_pf of the last service() calls
-                if (!chkl && !pf_loaded && s_pf == n + 1) { load_pf(n + 1); pf_loaded = true; }   // (not across the check: registers)
                 // ---- epilogue: U_{k+1}^n = U_k^n + du^n (du^n stays in x as the next carry)
                 {
                     double* Un = S.U + (size_t)((k + 1) % B) * nt * ns + (size_t)(n - 1) * ns;
                     double d2 = 0.0, dm = 0.0;
                     #pragma unroll
                     for (int r = 0; r < HH; ++r) {
-                        double2 v = lswap(*reinterpret_cast<const double2*>(ub + (size_t)r * NXU + c0));
-                        v.x += x[r][0];
-                        v.y += x[r][1];
+                        double2 v;
+                        v.x = ub[(size_t)r * NXU + uo0] + x[r][0];
+                        v.y = ub[(size_t)r * NXU + uo1] + x[r][1];
                         *reinterpret_cast<double2*>(Un + (size_t)(rg0 + r) * NXU + c0) = lswap(v);
                         d2 = fma(x[r][0], x[r][0], fma(x[r][1], x[r][1], d2));
                         dm = fmax(dm, fmax(fabs(x[r][0]), fabs(x[r][1])));
@@ -463,22 +467,6 @@ struct PsEngine {
                         }
                     }
                 }
-                // ---- the next level's u rows if they are not loaded yet (levels with a residual check, or set p-1 had not
-                //      published them): thread 0 waits for set p-1's counters.  pf_loaded is CTA-uniform: s_pf was read
-                //      right behind a barrier, and thread 0 calls service() again only behind the next one.
-                if (!pf_loaded) {
-                    cbar();                                         // every thread's U_{k+1}^n rows are stored: service() may publish them
-                    if (tid == 0) {
-                        for (;;) {
-                            service(fbase);
-                            if (!pf_lv) break;
-                            __nanosleep(64);
-                        }
-                    }
-                    cbar();
-                    load_pf(n + 1);
-                }
-                cbar();                                             // every thread is done reading this level's u
             }
             // ---- pass end: every set done; wait for the decisions of this pass's iterations
             __syncthreads();          // (A)

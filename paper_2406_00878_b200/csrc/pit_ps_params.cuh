@@ -30,6 +30,7 @@ struct PsParams {
     // LAW 1 coefficients of A_n = I + tau dF/du (host-computed, so the kernel reads them from the constant bank):
     // a_E = ax u_E - bx, a_W = -ax u_W - bx, a_N = ay u_N - by, a_S = -ay u_S - by, a_C = aC1
     double ax, bx, ay, by, aC1, invC1;
+    int dbg;                    // developer experiments (PIT_PS_DBG; 0 = product path): bit 0 = do not wait for LL cells (wrong results, timing only)
 };
 
 // Implemented in pit_ps_law1.cu: the engine-5 kernel for (row length, base strip height), its dynamic shared memory
