@@ -188,9 +188,11 @@ def exchange_floor(st, ei, nt, t_newton):
     """Engine 4's latency floor: every level solve of a warp group is a chain of 2 S dependent neighbour exchanges
     (one per half-sweep); a group runs passes x nt levels one after another, so the solve cannot beat
     levels_per_group x 2 S hops at the isolated hop latency."""
-    if ei.get("engine") != 4:
+    if ei.get("engine") not in (4, 5):
         return None
-    levels = st["steps"]                      # levels processed by one warp group (passes x nt)
+    levels = st["steps"]                      # levels processed by one warp group / CTA set (passes x nt)
+    if ei["engine"] == 5:
+        levels += st["depth"] - 1             # set p starts one level behind set p-1: the chain through all D sets
     hops = levels * 2 * ei["sweeps"]
     ms = hops * HOP_US * 1e-3
     return {"levels_per_group": levels, "hops_on_chain": hops, "us_per_hop_isolated": HOP_US, "ms": ms,
@@ -410,18 +412,20 @@ def main():
                    "newton_iterations": nit, "status": status, "pipeline_depth": st["depth"], "grid_ctas": st["grid"],
                    "l2": f"inputs larger than L2 (U = {p.dof * 8 / 1e9:.2f} GB per iterate buffer)",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": ("k_newton_nb (engine 4, persistent: a+b+c+d fused)" if ei["engine"] == 4
-                                                else "k_newton_col (engine 3, persistent: a+b+c+d fused)"), "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": {5: "k_newton_ps (engine 5, persistent: a+b+c+d fused)",
+                                           4: "k_newton_nb (engine 4, persistent: a+b+c+d fused)"}.get(
+                                               ei["engine"], "k_newton_col / k_newton_onchip (engines 3 / 2, persistent: a+b+c+d fused)"),
+                     "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "algorithmic": f"{BYTES_PER_DOF_IT} B per DOF per Newton iteration (SURVEY 8(d) fused minimum)"},
         "kernels": {"k_newton_ms": t_newton * 1e3, "engine": ei["engine"],
-                    "level_solver": ({"method": "red-black SOR, fixed sweeps (engine 4)", "sweeps": ei["sweeps"],
+                    "level_solver": ({"method": f"red-black SOR, fixed sweeps (engine {ei['engine']})", "sweeps": ei["sweeps"],
                                       "omega": ei["omega"], "jacobi_bound_q": ei["q"], "pipeline_depth": st["depth"],
                                       "levels_per_group": st["steps"],
                                       "rel_level_residual_per_newton_it": [r for r, _ in ei["linres"][:nit]]}
-                                     if ei["engine"] == 4 else
-                                     {"method": "Jacobi-scaled BiCGSTAB (engine 3)", "wavefront_steps": st["steps"],
+                                     if ei["engine"] in (4, 5) else
+                                     {"method": f"Jacobi-scaled BiCGSTAB (engine {ei['engine']})", "wavefront_steps": st["steps"],
                                       "bicgstab_iterations": st["inner_iterations"]}),
                     "sync_floor": sync_floor(st, nit, t_newton),
                     "exchange_floor": exchange_floor(st, ei, p.nt, t_newton),

@@ -42,6 +42,7 @@
  *             PIT_X0=0           engines 2-3 start each level solve from 0 instead of the carry du^{n-1}
  *             PIT_MERGE=0        engine 3 without the merged first BiCGSTAB iteration
  *             PIT_GUESS_GRAPH=0  the coarse-grid guess's level march without a CUDA graph
+ *             PIT_PS_DBG=1       engine 5 timing experiment: neighbour cells are not waited for (WRONG results)
  *           All NVTX ranges ("pit_solve_device", "pit_solve", ...) are emitted unconditionally (free without a tool).
  */
 #ifndef PIT_H
@@ -99,14 +100,20 @@ typedef struct {
                               the whole horizon (EXPLICIT) */
     int32_t pipeline_depth;/* Newton iterations in flight in the level wavefront; 0 = auto */
     int32_t device;        /* CUDA device ordinal */
-    int32_t engine;        /* Newton-solve engine.  0 = auto: 4 if it applies, else 3, 2, 1 (the first that fits).
+    int32_t engine;        /* Newton-solve engine.  0 = auto: 5 if it applies, else 4, 3, 2, 1 (the first that fits).
                               1 = global-state engine (any size), 2 = strip on-chip engine, 3 = column-blocked
                               on-chip engine (nx = 256 or 512 unknowns per row) — engines 1-3 solve every level
                               with Jacobi-scaled BiCGSTAB to lin_rtol behind grid-wide barriers;
                               4 = neighbour-synchronised engine: every level solved by lin_sweeps red-black SOR
                               sweeps (Young's relaxation from the Jacobi bound of A_1 at the initial iterate),
                               only neighbouring row strips synchronise (64..512 unknowns per row, even; periodic
-                              grids also need an even number of rows; <= 4 rows per CTA).  2/3/4: PIT_EINVAL if
+                              grids also need an even number of rows; <= 4 rows per CTA);
+                              5 = pipeline of CTA sets: set p (sms / D CTAs) runs Newton iteration p over the levels one
+                              level behind set p-1, D = pipeline_depth iterations in flight; a CTA keeps its strip of
+                              rows of a level on chip (du in registers, u^n and b in shared memory), the level solves are
+                              engine 4's red-black SOR sweeps, strips of a set meet through neighbour exchange only
+                              (constant-viscosity Burgers, periodic, 256 or 512 unknowns per row, even row count, strip
+                              heights that have an instantiation: pit_newton_ps.cuh).  2/3/4/5: PIT_EINVAL if
                               they do not apply.  Level solves outside the Newton solve (pit_level_solve_device,
                               the product forms) always use BiCGSTAB (engines 1-3). */
     int32_t guess_cf;      /* initial Newton iterate when the caller passes no guess:
@@ -233,7 +240,8 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * out[2] = pipeline depth used, out[3] = grid CTAs, out[4] = kernel launches of the last solve,
  * out[5] = device time of the persistent Newton kernel of the last solve [ns] (CUDA events on the
  * launching stream), out[6] = device time of the iterate-initialisation kernel [ns], out[7] = engine
- * (1 global-state, 2 strip on-chip, 3 column-blocked on-chip), out[8..14] = on-chip engine cycle accounting summed over CTAs
+ * (1 global-state, 2 strip on-chip, 3 column-blocked on-chip, 4 neighbour-synchronised, 5 pipeline of CTA sets; for
+ * 4 and 5 out[0] = levels one CTA processed, out[2] / out[3] = the depth and CTAs the kernel ran with), out[8..14] = on-chip engine cycle accounting summed over CTAs
  * (prologue, phase 1, phase 2, epilogue, grid barriers, scalar reductions, step bookkeeping) when the
  * environment variable PIT_TRACE was set at pit_create (zeros otherwise), out[15] = 1 if the last solve
  * inverted Eq. (6) with the (b2) product form (inverse_mode PRODUCT_WINDOW, or AUTO with the whole horizon
@@ -243,10 +251,10 @@ int pit_sizes(const pit_handle* h, int64_t* ns, int64_t* device_bytes);
  * initial guess (coarse solve + interpolation) [ns], 0 without it. */
 int pit_stats(pit_handle* h, int64_t* out, int32_t n);
 
-/* Engine facts of the last Newton solve (synchronizes with it).  out[0] = engine (1..4), out[1] = omega,
- * out[2] = sweeps per level solve, out[3] = the Jacobi bound q (engine 4; 0 otherwise), then for k = 0..n_iter-1:
+/* Engine facts of the last Newton solve (synchronizes with it).  out[0] = engine (1..5), out[1] = omega,
+ * out[2] = sweeps per level solve, out[3] = the Jacobi bound q (engines 4 and 5; 0 otherwise), then for k = 0..n_iter-1:
  * out[4 + 2k] = ||res||_2 / ||b||_2 of iteration k's level solves over all levels (res = b - A_n du^n, b = r^n +
- * du^{n-1}), out[5 + 2k] = max |res| (engine 4 only; zeros otherwise).  n = number of doubles out can hold. */
+ * du^{n-1}), out[5 + 2k] = max |res| (engines 4 and 5; zeros otherwise).  n = number of doubles out can hold. */
 int pit_engine_info(pit_handle* h, double* out, int32_t n);
 
 const char* pit_strerror(int code);

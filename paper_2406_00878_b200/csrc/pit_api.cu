@@ -1288,7 +1288,8 @@ int pit_stats(pit_handle* h, int64_t* out, int32_t n) {
     }
     unsigned long long tr[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (h->trace) CUDA_TRY(h, cudaMemcpy(tr, h->trace, sizeof(tr), cudaMemcpyDeviceToHost));
-    const long long v[17] = {s[0], s[1], h->D, h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
+    const bool nbps = h->last_engine == 4 || h->last_engine == 5;      // these kernels report their own depth and grid
+    const long long v[17] = {s[0], s[1], nbps ? s[2] : h->D, nbps ? s[3] : h->G, h->launches, (long long)(t_newton * 1e6), (long long)(t_init * 1e6),
                              h->last_engine ? h->last_engine : h->engine, (long long)tr[0], (long long)tr[1], (long long)tr[2], (long long)tr[3],
                              (long long)tr[4], (long long)tr[5], (long long)tr[6], (long long)h->product_used, s[4]};
     for (int i = 0; i < n && i < 17; ++i) out[i] = v[i];

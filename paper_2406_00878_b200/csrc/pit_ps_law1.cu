@@ -13,7 +13,8 @@ static const void* ps_inst(size_t* smem, int* threads) {
 
 // Instantiated shapes: (row length, base strip height HE); a set's strips have HE or HE + 2 rows.
 const void* ps_kernel_law1(int nxu, int he, size_t* smem, int* threads) {
-    if (nxu == 512 && he == 20) return ps_inst<512, 20>(smem, threads);
+    if (nxu == 512 && he == 20) return ps_inst<512, 20>(smem, threads);     // BASELINE c5: 6 sets of 24 strips
+    if (nxu == 256 && he == 14) return ps_inst<256, 14>(smem, threads);     // BASELINE c4: 8 sets of 18 strips
     return nullptr;
 }
 
