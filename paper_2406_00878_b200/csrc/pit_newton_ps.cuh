@@ -68,7 +68,7 @@ struct PsEngine {
     // column ^ f), so that the colour of local point (q, jj) is (q + jj) & 1 in both groups and every register
     // subscript stays compile-time; the E/W roles then mirror, which only flips the sign of ax and the shuffle
     // direction (per-thread constants).
-    template <int HH>
+    template <int HH, bool ISO>
     __device__ __forceinline__ static void run(const PsParams& S, double* sm) {
         constexpr int H = 2 * HH;
         const Prob P = S.P;
@@ -114,12 +114,17 @@ struct PsEngine {
         const double oic = omega * S.invC1, om1 = 1.0 - omega;     // x <- om1 x + oic (b - offdiag x)
         // kind A rows (other colour in local column 1): the product travels to thread t + 1 (f = 0) or t - 1 (f = 1);
         // kind B rows (other colour in local column 0): the opposite way.
-        const int srcA = (lane + (f ? 1 : 31)) & 31, srcB = (lane + (f ? 31 : 1)) & 31;
+        int srcA = (lane + (f ? 1 : 31)) & 31, srcB = (lane + (f ? 31 : 1)) & 31;
+        asm volatile("" : "+r"(srcA), "+r"(srcB));
         const int edgeA = f ? 31 : 0, edgeB = f ? 0 : 31;    // lanes whose source lies in the neighbouring warp
         const int wsA = f ? (wl + 1) % NW : (wl + NW - 1) % NW, wsB = f ? (wl + NW - 1) % NW : (wl + 1) % NW;
         double* wdA = wedge;                                 // [HHM][NW]
         double* wdB = wedge + (size_t)HHM * NW;
-        const int isA = lane == edgeA, isB = lane == edgeB;
+        int isA = lane == edgeA, isB = lane == edgeB;         // this lane's kind A / B source lies in the neighbouring warp
+        int wrA = lane == 31 - edgeA, wrB = lane == 31 - edgeB;   // this lane's kind A / B product is a neighbouring warp's source
+        unsigned wdA_w = (unsigned)__cvta_generic_to_shared(wdA + wl), wdB_w = (unsigned)__cvta_generic_to_shared(wdB + wl);
+        // (opaque to the compiler, which otherwise rebuilds these from the thread index in every row of the sweeps)
+        asm volatile("" : "+r"(isA), "+r"(isB), "+r"(wrA), "+r"(wrB), "+r"(wdA_w), "+r"(wdB_w));
         // ubuf rows are de-interleaved: [even columns (T)][odd columns (T)], so that a warp's loads of one local column
         // are contiguous (no bank conflicts).  Offsets of local columns 0 and 1, and of their out-of-thread x-neighbours
         // (actual column c0 - 1: odd, pair t - 1; actual column c0 + 2: even, pair t + 1; periodic).
@@ -193,21 +198,31 @@ struct PsEngine {
             for (int q = 0; q < HH; ++q) {
                 const int jn = 1 - ((q + cc) & 1);               // the other colour's local column in this row
                 const double uq = ub[(size_t)q * NXU + (jn ? uo1 : uo0)], xq = x[q][jn];
-                const double m = uq * xq, bxq = bx * xq, byq = by * xq;
-                const double pa = fma(a1, m, -bxq), pb = fma(-a1, m, -bxq);
-                const double pn = fma(ay, m, -byq), psv = fma(-ay, m, -byq);
+                // (a1 u - bx) x and (-a1 u - bx) x = -(a1 u - bx) x - 2 bx x; the same in y (on an isotropic grid the y
+                // products ARE the x products: the +a form is pa unless the columns are swapped)
+                const double pa = fma(a1, uq, -bx) * xq, pb = fma(-2.0 * bx, xq, -pa);
+                double pn, psv;
+                if (ISO) {
+                    pn = f ? pb : pa;
+                    psv = f ? pa : pb;
+                } else {
+                    pn = fma(ay, uq, -by) * xq;
+                    psv = fma(-2.0 * by, xq, -pn);
+                }
                 // the travelling product goes to the neighbouring thread at once (shuffle); the lanes whose source lies in
                 // the neighbouring warp take theirs from shared memory behind the barrier instead
                 if (jn == 1) {               // kind A: in-thread term pa, travelling term pb
                     const double in = __shfl_sync(0xffffffffu, pb, srcA);
                     tt[q] -= pa;
                     if (!isA) tt[q] -= in;
-                    if (lane == 31 - edgeA) wdA[q * NW + wl] = pb;
+                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
+                                 ::"r"(wdA_w + (unsigned)(q * NW * 8)), "d"(pb), "r"(wrA) : "memory");
                 } else {                     // kind B: in-thread term pb, travelling term pa
                     const double in = __shfl_sync(0xffffffffu, pa, srcB);
                     tt[q] -= pb;
                     if (!isB) tt[q] -= in;
-                    if (lane == 31 - edgeB) wdB[q * NW + wl] = pa;
+                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
+                                 ::"r"(wdB_w + (unsigned)(q * NW * 8)), "d"(pa), "r"(wrB) : "memory");
                 }
                 if (q > 0) tt[q > 0 ? q - 1 : 0] -= pn;
                 else if (g == 1) gx[T + t] = pn;             // to the lower group's top row
@@ -537,7 +552,12 @@ __global__ void __launch_bounds__(NXU, 1) k_newton_ps(const PsParams S) {
     if ((int)blockIdx.x >= S.D * S.Gs) return;
     const int s = blockIdx.x % S.Gs;
     const int na = (S.P.nyu - HE * S.Gs) / 2;
-    if (s < na) E::template run<HE / 2 + 1>(S, sm_ps); else E::template run<HE / 2>(S, sm_ps);
+    const bool iso = S.ax == S.ay && S.bx == S.by;      // hx = hy: the y products of the sweeps are the x products
+    if (s < na) {
+        if (iso) E::template run<HE / 2 + 1, true>(S, sm_ps); else E::template run<HE / 2 + 1, false>(S, sm_ps);
+    } else {
+        if (iso) E::template run<HE / 2, true>(S, sm_ps); else E::template run<HE / 2, false>(S, sm_ps);
+    }
 }
 
 }  // namespace pit

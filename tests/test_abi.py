@@ -70,7 +70,7 @@ def test_strerror(built):
 @pytest.mark.parametrize("field,value", [("abi_version", 7), ("nx", 1), ("nt", 0), ("dt", 0.0), ("m0", -1.0),
                                          ("newton_max", 0), ("pipeline_depth", 99), ("bc", 5),
                                          ("guess_cf", 1), ("guess_cf", 5), ("guess_cf", -2), ("stop_norm", 2),
-                                         ("engine", 5), ("lin_sweeps", -1), ("lin_sweeps", 401), ("lin_check", -1)])
+                                         ("engine", 6), ("lin_sweeps", -1), ("lin_sweeps", 401), ("lin_check", -1)])
 def test_invalid_config_rejected_before_touching_the_gpu(built, field, value):
     c = pit.make_config(W.config(1))
     setattr(c, field, value)
