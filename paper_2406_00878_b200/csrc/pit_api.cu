@@ -79,6 +79,7 @@ struct pit_handle {
     bool nb = false;              // the Newton solve runs on engine 4
     int nb_rmax = 0, nb_G = 0, nb_D = 0, nb_dm = 0;   // base strip height, CTAs, iterations in flight, warp groups
     int nb_threads = 0;                               // threads per CTA
+    int nb_want = 0;                                  // warp groups asked of the instantiation table (0 = the shape's default)
     bool nb_ctl_ready = false;                        // slab iterations: omega / sweeps fixed at the first call
     size_t nb_smem = 0;
     unsigned long long* nb_llx = nullptr;   // LL cells, x publications
@@ -486,7 +487,10 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
         const int hb4 = P.nyu / G4;
         size_t smem4 = 0;
         int occ4 = 0, dm = 1, thr4 = 0;
-        const void* fn = nb_fn(hb4, law, P.nxu, c.pipeline_depth, &smem4, &dm, &thr4);
+        // rows of 256 unknowns, one row per CTA: six warp groups by default (a six-iteration solve in one pass of the
+        // level wavefront: c3 63.8 -> 50.0 ms), else the shape's default build
+        h->nb_want = c.pipeline_depth > 0 ? c.pipeline_depth : ((P.nxu == 256 && hb4 == 1 && c.newton_max >= 6) ? 6 : 0);
+        const void* fn = nb_fn(hb4, law, P.nxu, h->nb_want, &smem4, &dm, &thr4);
         const int D4 = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : dm, std::min(dm, c.newton_max)));
         const int rmax = hb4;
         if (fn && smem4 <= 227 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4) == cudaSuccess &&
@@ -746,7 +750,7 @@ static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, doub
     void* args[] = {(void*)&S};
     size_t smem4 = 0;
     int dm4 = 0, thr4 = 0;
-    const void* fn = nb_fn(h->nb_rmax, h->law, P.nxu, h->cfg.pipeline_depth, &smem4, &dm4, &thr4);
+    const void* fn = nb_fn(h->nb_rmax, h->law, P.nxu, h->nb_want, &smem4, &dm4, &thr4);
     CUDA_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->nb_smem));
     CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->nb_G), dim3(h->nb_threads), args, h->nb_smem, st));
     CUDA_TRY(h, cudaEventRecord(h->ev[3], st));

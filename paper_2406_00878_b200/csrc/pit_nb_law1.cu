@@ -19,6 +19,8 @@ const void* nb_kernel_law1(int hb, int nxu, int want_dm, size_t* smem, int* dm, 
         case 64: return hb == 1 ? nb_inst<1, 64, 4, 2>(smem, dm, threads) : nullptr;
         case 128: return hb == 1 ? nb_inst<1, 128, 4, 2>(smem, dm, threads) : nullptr;
         case 256:
+            if (want_dm == 6)      // six groups of 128 threads: the six iterations of a c3-like solve in one pass
+                return hb == 1 ? nb_inst<1, 256, 6, 2>(smem, dm, threads) : nullptr;
             return hb == 1 ? nb_inst<1, 256, 4, 2>(smem, dm, threads)
                            : (hb == 2 ? nb_inst<2, 256, 4, 2>(smem, dm, threads) : nullptr);
         case 512:

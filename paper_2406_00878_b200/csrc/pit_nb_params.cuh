@@ -8,7 +8,7 @@ namespace pit {
 constexpr int NB_RX = 8;     // LL ring entries per CTA and group for x publications (a group's consumer lags <= 2)
 constexpr int NB_RU = 8;     // LL ring entries per CTA and group for U boundary-row publications (one per level)
 constexpr int NB_LAG = 4;    // a group may finish at most NB_LAG levels ahead of the next group (< NB_RU - 1)
-constexpr int NB_DMAX = 4;   // Newton iterations in flight (upper bound; per instantiation DM <= NB_DMAX)
+constexpr int NB_DMAX = 6;   // Newton iterations in flight (upper bound; per instantiation DM <= NB_DMAX)
 constexpr int NB_NP = 7;     // per-CTA partials per Newton iteration: sum r^2, max|r|, sum du^2, max|du|,
                              // sum res^2, max|res| (level-solve residuals), sum b^2 (level right-hand sides)
 __host__ __device__ constexpr bool nb_is_max(int j) { return j == 1 || j == 3 || j == 5; }

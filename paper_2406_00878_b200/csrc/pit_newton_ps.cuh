@@ -112,6 +112,7 @@ struct PsEngine {
         const double a1 = f ? -S.ax : S.ax;                  // ax seen through the column swap
         const double sx2 = f ? -P.i2hx : P.i2hx;             // 1/(2 hx) seen through the column swap (residual)
         const double oic = omega * S.invC1, om1 = 1.0 - omega;     // x <- om1 x + oic (b - offdiag x)
+        const double rsc = aC1 * (om1 / omega);                      // residual of a just-relaxed point: rsc (x_new - x_old)
         // kind A rows (other colour in local column 1): the product travels to thread t + 1 (f = 0) or t - 1 (f = 1);
         // kind B rows (other colour in local column 0): the opposite way.
         int srcA = (lane + (f ? 1 : 31)) & 31, srcB = (lane + (f ? 31 : 1)) & 31;
@@ -344,24 +345,30 @@ struct PsEngine {
                     for (int cc = 0; cc < 2; ++cc) {
                         double tt[HH];
                         gather(cc, tt, true, fbase);
-                        double rs2 = 0.0, rsm = 0.0;
-                        #pragma unroll
-                        for (int i = 0; i < HH; ++i) {
-                            const int r = i == 0 ? 0 : (i == 1 ? HH - 1 : i - 1);     // the two end rows first: one of them is the strip's boundary row
-                            const int j = (r + cc) & 1;
-                            const double xo = x[r][j], xn = fma(oic, tt[r], om1 * xo);
-                            x[r][j] = xn;
-                            if (cc == 1 && lastm) {
-                                const double rr = aC1 * (om1 / omega) * (xn - xo);
+                        if (cc == 1 && lastm) {      // (CTA-uniform) the last black half-sweep of a checked level: also its residual
+                            double rs2 = 0.0, rsm = 0.0;
+                            #pragma unroll
+                            for (int r = 0; r < HH; ++r) {
+                                const int j = (r + cc) & 1;
+                                const double xo = x[r][j], xn = fma(oic, tt[r], om1 * xo);
+                                x[r][j] = xn;
+                                const double rr = rsc * (xn - xo);
                                 rs2 = fma(rr, rr, rs2);
                                 rsm = fmax(rsm, fabs(rr));
                             }
-                            if (i == (HH > 1 ? 1 : 0))       // publish: local row 0 of the lower group, HH-1 of the upper group
-                                ll_put(mycell(qx), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
-                        }
-                        if (cc == 1 && lastm) {
+                            ll_put(mycell(qx), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
                             ac(4) += rs2;
                             ac(5) = fmax(ac(5), rsm);
+                        } else {
+                            #pragma unroll
+                            for (int i = 0; i < HH; ++i) {
+                                const int r = i == 0 ? 0 : (i == 1 ? HH - 1 : i - 1);     // the two end rows first: one of them is the strip's boundary row
+                                const int j = (r + cc) & 1;
+                                const double xo = x[r][j];
+                                x[r][j] = fma(oic, tt[r], om1 * xo);
+                                if (i == (HH > 1 ? 1 : 0))       // publish: local row 0 of the lower group, HH-1 of the upper group
+                                    ll_put(mycell(qx), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
+                            }
                         }
                         lastx = (int)qx;
                         ++qx;

@@ -13,9 +13,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--solves", type=int, default=1)
 ap.add_argument("--depth", type=int, default=0)
+ap.add_argument("--guess-cf", type=int, default=0)
+ap.add_argument("--nt", type=int, default=0)
 a = ap.parse_args()
-p = W.config(a.config)
-s = pit.Solver(p, pipeline_depth=a.depth)
+p = W.config(a.config, nt=a.nt or None)
+s = pit.Solver(p, pipeline_depth=a.depth, guess_cf=a.guess_cf)
 d_u0 = torch.from_numpy(p.u0).cuda()
 d_out = torch.empty((p.nt, p.ns), dtype=torch.float64, device="cuda")
 d_hist = torch.zeros((s.cfg.newton_max, 4), dtype=torch.float64, device="cuda")
