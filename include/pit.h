@@ -176,7 +176,8 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
  *   d_info [2] int32 = { n_iter, status } written on the device at the end of the solve.
  *   cuda_stream: a cudaStream_t (NULL = legacy default stream).
  * The return value reports only argument / launch errors; the solve status is d_info[1] once the
- * stream work completes. */
+ * stream work completes.  d_u_out is the library's to write from the first kernel on: engine 5 keeps the iterate it
+ * expects to be the last one there (no final copy), so its contents are unspecified until the stream work completes. */
 int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, const double* d_guess,
                      double* d_u_out, double* d_hist, int32_t* d_info, void* cuda_stream);
 

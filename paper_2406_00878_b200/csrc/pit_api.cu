@@ -96,6 +96,7 @@ struct pit_handle {
     size_t ps_smem = 0;
     unsigned long long* ps_llx = nullptr;   // [D][Gs][PS_RX][2][nxu / 2] LL cells
     unsigned* ps_lvl = nullptr;             // [D][Gs] level counters
+    int* ps_hint = nullptr;                 // device word: Newton iterations of the previous engine-5 solve (0 = none)
     size_t ps_llx_bytes = 0;
     int last_engine = 0;          // engine of the last Newton solve
     // developer switches (pit.h "Debug environment"), read once at pit_create so a handle never changes path
@@ -216,8 +217,8 @@ static void free_all(pit_handle* h) {
     dfree(h, h->ex_B); dfree(h, h->ex_C5); dfree(h, h->ex_err);
     dfree(h, h->nb_llx); dfree(h, h->nb_llu); dfree(h, h->nb_hpart); dfree(h, h->nb_sync); dfree(h, h->nb_qbits);
     dfree(h, h->nb_ctl); dfree(h, h->nb_linres);
-    dfree(h, h->ps_llx); dfree(h, h->ps_lvl);
-    h->ps_llx = nullptr; h->ps_lvl = nullptr;
+    dfree(h, h->ps_llx); dfree(h, h->ps_lvl); dfree(h, h->ps_hint);
+    h->ps_llx = nullptr; h->ps_lvl = nullptr; h->ps_hint = nullptr;
     h->nb_llx = h->nb_llu = nullptr; h->nb_hpart = h->nb_ctl = h->nb_linres = nullptr; h->nb_sync = nullptr;
     h->nb_qbits = nullptr;
     h->ex_B = h->ex_C5 = nullptr; h->ex_err = nullptr; h->ex_capB = h->ex_capC = 0;
@@ -554,7 +555,8 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
         (h->nb && ((rc = dalloc(h, &h->nb_llx, (size_t)h->nb_G * h->nb_dm * NB_RX * 2 * (P.nxu / 2) * 2)) ||
                    (rc = dalloc(h, &h->nb_llu, (size_t)h->nb_G * h->nb_dm * NB_RU * 2 * P.nxu * 2)))) ||
         (h->ps && ((rc = dalloc(h, &h->ps_llx, (size_t)h->ps_D * h->ps_Gs * PS_RX * 2 * (P.nxu / 2) * 2)) ||
-                   (rc = dalloc(h, &h->ps_lvl, (size_t)h->ps_D * h->ps_Gs)))) ||
+                   (rc = dalloc(h, &h->ps_lvl, (size_t)h->ps_D * h->ps_Gs)) ||
+                   (rc = dalloc(h, &h->ps_hint, 1)))) ||
         ((h->nb || h->ps) && ((rc = dalloc(h, &h->nb_hpart, (size_t)MAXK * std::max(h->nb_G, h->ps_Gs) * NB_NP)) ||
                    (rc = dalloc(h, &h->nb_sync, (size_t)2 * MAXK)) ||
                    (rc = dalloc(h, &h->nb_qbits, 1)) ||
@@ -570,7 +572,8 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
     bool ev_ok = true;
     for (auto& e : h->ev) ev_ok = ev_ok && cudaEventCreate(&e) == cudaSuccess;
     if (!ev_ok || (!measure && (cudaMemset(h->bar, 0, sizeof(GridBar)) != cudaSuccess ||
-                                cudaMemset(h->stats, 0, (8 + MAXK) * sizeof(long long)) != cudaSuccess))) {
+                                cudaMemset(h->stats, 0, (8 + MAXK) * sizeof(long long)) != cudaSuccess ||
+                                (h->ps_hint && cudaMemset(h->ps_hint, 0, sizeof(int)) != cudaSuccess)))) {
         cudaGetLastError();
         free_all(h);
         delete h;
@@ -760,7 +763,8 @@ static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, doub
 }
 
 // Engine 5: omega and the sweep count as engine 4 (k_nb_q / k_nb_ctl), then the persistent pipeline-of-sets kernel.
-static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double* d_hist, int* d_info, cudaStream_t st) {
+static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double* d_hist, int* d_info, cudaStream_t st,
+                     bool u0_bcast) {
     NvtxRange nvtx_("engine5 k_newton_ps");
     const Prob& P = h->P;
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
@@ -770,7 +774,7 @@ static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double*
     CUDA_TRY(h, cudaMemsetAsync(h->nb_linres, 0, sizeof(double) * 2 * MAXK, st));
     CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_qbits, 0, sizeof(unsigned long long), st));
-    nb_setup_launch(P, h->U, nullptr, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
+    nb_setup_launch(P, u0_bcast ? d_u0 : h->U, nullptr, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
                     std::max(1, std::min(grid_for(P.ns, h->sms), 2 * h->sms)), st);
     CUDA_TRY(h, cudaGetLastError());
     PsParams S;
@@ -786,6 +790,8 @@ static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double*
     S.ax = P.dt * P.i2hx; S.bx = P.dt * P.m0 * P.ihx2; S.ay = P.dt * P.i2hy; S.by = P.dt * P.m0 * P.ihy2;
     S.aC1 = 1.0 + 2.0 * (S.bx + S.by); S.invC1 = 1.0 / S.aC1;
     S.dbg = h->dbg.ps_dbg;
+    S.u0_bcast = u0_bcast ? 1 : 0;
+    S.hint = h->ps_hint;
     void* args[] = {(void*)&S};
     size_t smem5 = 0;
     int thr5 = 0;
@@ -1005,9 +1011,15 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
     h->launches = 0;
     h->guess_timed = false;
     int rc;
+    // engine 5 reads the broadcast u^0 itself: U_0 = u^0 at every level is not materialised
+    const bool ps_bcast = h->ps && !d_guess && !h->coarse && !want_product(h, d_bc, st);
     if (!d_guess && h->coarse) {
         if ((rc = build_guess(h, d_u0, d_bc, st)) != PIT_OK) return rc;
         CUDA_TRY(h, cudaEventRecord(h->ev[0], st));       // U_0 is already in place: no init kernel
+        CUDA_TRY(h, cudaEventRecord(h->ev[1], st));
+        h->timed = true;
+    } else if (ps_bcast) {
+        CUDA_TRY(h, cudaEventRecord(h->ev[0], st));
         CUDA_TRY(h, cudaEventRecord(h->ev[1], st));
         h->timed = true;
     } else if ((rc = launch_init(h, d_u0, d_guess, st)) != PIT_OK) {
@@ -1020,7 +1032,7 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
         CUDA_TRY(h, cudaMemcpyAsync(h->d_u0, d_u0, sizeof(double) * h->P.ns, cudaMemcpyDeviceToDevice, st));
         d_u0 = h->d_u0;
     }
-    if (h->ps) return launch_ps(h, d_u0, d_u_out, d_hist, (int*)d_info, st);
+    if (h->ps) return launch_ps(h, d_u0, d_u_out, d_hist, (int*)d_info, st, ps_bcast);
     if (h->nb) return launch_nb(h, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_u_out, d_hist, (int*)d_info, st);
     SolveParams S = base_params(h);
     S.u0 = d_u0;
@@ -1082,8 +1094,13 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     h->launches = 0;
     h->guess_timed = false;
     int rc;
+    const bool ps_bcast = h->ps && !guess && !h->coarse && !want_product(h, has_bc ? h->d_bc : nullptr, 0);
     if (!guess && h->coarse) {
         if ((rc = build_guess(h, h->d_u0, has_bc ? h->d_bc : nullptr, 0)) != PIT_OK) return rc;
+        CUDA_TRY(h, cudaEventRecord(h->ev[0], 0));
+        CUDA_TRY(h, cudaEventRecord(h->ev[1], 0));
+        h->timed = true;
+    } else if (ps_bcast) {
         CUDA_TRY(h, cudaEventRecord(h->ev[0], 0));
         CUDA_TRY(h, cudaEventRecord(h->ev[1], 0));
         h->timed = true;
@@ -1096,7 +1113,7 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     if (prod) {
         rc = solve_product(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else if (h->ps) {
-        rc = launch_ps(h, h->d_u0, nullptr, h->hist, h->info, 0);
+        rc = launch_ps(h, h->d_u0, nullptr, h->hist, h->info, 0, ps_bcast);
     } else if (h->nb) {
         rc = launch_nb(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else {

@@ -30,6 +30,8 @@ struct PsParams {
     // LAW 1 coefficients of A_n = I + tau dF/du (host-computed, so the kernel reads them from the constant bank):
     // a_E = ax u_E - bx, a_W = -ax u_W - bx, a_N = ay u_N - by, a_S = -ay u_S - by, a_C = aC1
     double ax, bx, ay, by, aC1, invC1;
+    int u0_bcast;               // 1: U_0 = u^0 at every level and was NOT materialised in ring buffer 0 (iteration 0 reads u0)
+    int* hint;                  // device word: Newton iterations of the previous solve on this handle (0 = none)
     int dbg;                    // developer experiments (PIT_PS_DBG; 0 = product path): bit 0 = do not wait for LL cells (wrong results, timing only)
 };
 

@@ -132,3 +132,40 @@ def test_engine5_enoconv_and_sweeps_override():
     U, hist, nit, st, _ = _sol(p, lin_sweeps=1)        # one sweep per level: inexact, more Newton iterations
     U2, hist2, nit2, st2, _ = _sol(p)
     assert st in (0, 1) and nit >= nit2 and normwise_rel(U, U2) <= 1e-10
+
+
+def test_engine5_repeated_solves_on_one_handle():
+    """The second solve on a handle writes its probable final iterate straight into u_out (the ring slot the previous
+    solve ended in) and reads the broadcast u^0 instead of a materialised U_0: same bits as the first solve; when the
+    iteration count changes (other data: the guess of the slot is wrong) the result equals a fresh handle's; a
+    caller's guess goes through ring buffer 0 as before."""
+    from gpu_util import dev, torch_cuda
+    torch = torch_cuda()
+    p = W.config(5, nt=6)
+    s = pit.Solver(p, engine=5)
+
+    def run(solver, u0, guess=None):
+        d_out = torch.full((p.nt, p.ns), float("nan"), dtype=torch.float64, device="cuda")
+        d_hist = torch.zeros((solver.cfg.newton_max, 4), dtype=torch.float64, device="cuda")
+        d_info = torch.zeros(2, dtype=torch.int32, device="cuda")
+        solver.solve_device(dev(u0), None, None if guess is None else dev(guess), d_out, d_hist, d_info)
+        torch.cuda.synchronize()
+        return d_out.cpu().numpy(), d_hist.cpu().numpy(), d_info.cpu().tolist()
+
+    try:
+        U1, h1, i1 = run(s, p.u0)
+        U2, h2, i2 = run(s, p.u0)
+        assert i1 == i2 and i1[1] in (0, 1)
+        assert np.array_equal(U1, U2) and np.array_equal(h1, h2)
+        u0b = 0.25 * p.u0                                   # weaker nonlinearity: fewer iterations than the slot guess
+        U3, h3, i3 = run(s, u0b)
+        U4, h4, i4 = run(s, p.u0, guess=U1)                 # converged guess: one iteration
+        s2 = pit.Solver(p, engine=5)
+        try:
+            U3f, h3f, i3f = run(s2, u0b)
+        finally:
+            s2.close()
+        assert i3 == i3f and np.array_equal(U3, U3f) and np.array_equal(h3, h3f)
+        assert i4[1] in (0, 1) and i4[0] <= 2 and normwise_rel(U4, U1) <= 1e-12
+    finally:
+        s.close()
