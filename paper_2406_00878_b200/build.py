@@ -1,8 +1,8 @@
 """Build libpit.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-Four translation units compiled in parallel and linked into one shared library: pit_api.cu (the C ABI, engines
+Five translation units compiled in parallel and linked into one shared library: pit_api.cu (the C ABI, engines
 1-3, kernel (a), the product forms, the coarse guess) and the engine-4 instantiations pit_nb_law0.cu /
-pit_nb_law1.cu (pit_newton_nb.cuh) and the engine-5 instantiations pit_ps_law1.cu (pit_newton_ps.cuh).
+pit_nb_law1.cu (pit_newton_nb.cuh) and the engine-5 instantiations pit_ps_law1.cu (pit_newton_ps.cuh) and pit_ps_law0.cu (pit_newton_ps0.cuh).
 """
 from __future__ import annotations
 
@@ -13,9 +13,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpit.so")
-UNITS = ["pit_api.cu", "pit_nb_law1.cu", "pit_nb_law0.cu", "pit_ps_law1.cu"]
+UNITS = ["pit_api.cu", "pit_nb_law1.cu", "pit_nb_law0.cu", "pit_ps_law1.cu", "pit_ps_law0.cu"]
 SOURCES = UNITS + ["pit_kernels.cu", "pit_internal.cuh", "pit_newton_onchip.cuh", "pit_newton_col.cuh",
-                   "pit_guess.cuh", "pit_explicit.cuh", "pit_newton_nb.cuh", "pit_nb_params.cuh", "pit_newton_ps.cuh", "pit_ps_params.cuh"]
+                   "pit_guess.cuh", "pit_explicit.cuh", "pit_newton_nb.cuh", "pit_nb_params.cuh", "pit_newton_ps.cuh", "pit_newton_ps0.cuh", "pit_ps_params.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 

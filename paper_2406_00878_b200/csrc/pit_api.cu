@@ -96,6 +96,7 @@ struct pit_handle {
     size_t ps_smem = 0;
     unsigned long long* ps_llx = nullptr;   // [D][Gs][PS_RX][2][nxu / 2] LL cells
     unsigned* ps_lvl = nullptr;             // [D][Gs] level counters
+    int ps_rg = 2;                          // row groups per CTA (PIT_PS_DBG bit 2: the one-group experiment)
     int* ps_hint = nullptr;                 // device word: Newton iterations of the previous engine-5 solve (0 = none)
     size_t ps_llx_bytes = 0;
     int last_engine = 0;          // engine of the last Newton solve
@@ -302,6 +303,12 @@ static const void* onchip_fn(int ppt, bool trace, int law) {
 
 static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool measure, pit_handle** out);
 
+// Engine 5 kernel for the handle's law, boundary condition and row length at base strip height he.
+static const void* ps_fn(const pit_handle* h, int he, size_t* smem, int* threads) {
+    return h->law == 1 ? ps_kernel_law1(h->P.nxu, he, h->ps_rg, smem, threads)
+                       : ps_kernel_law0(h->P.nxu, he, h->P.bc == PIT_PERIODIC ? 1 : 0, smem, threads);
+}
+
 // The c_f-coarsened problem of the initial guess: N_x / c_f, N_y / c_f intervals, N_t / c_f levels
 // of step c_f dt, same law, domain and solver settings.  "Solving Eq. (FDS) sequentially": the nested handle is
 // a ONE-level problem; build_guess marches it level by level (u^0 of level m = the converged level m-1), so its
@@ -369,6 +376,7 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
         h->dbg.merge = env_int("PIT_MERGE", 1) != 0;
         h->dbg.guess_graph = env_int("PIT_GUESS_GRAPH", 1) != 0;
         h->dbg.ps_dbg = env_int("PIT_PS_DBG", 0);
+        h->ps_rg = (h->dbg.ps_dbg & 4) ? 1 : 2;
     }
     pit_config& c = h->cfg;
     if (c.lin_rtol == 0.0) c.lin_rtol = 1e-6;     // inexact-Newton forcing term (R10)
@@ -506,7 +514,7 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
     // strips with HE or HE + 2 rows each (HE even: every strip starts on an even row).  D = pipeline_depth, or the
     // largest depth <= min(8, newton_max) whose strips fit on chip.
     if ((c.engine == 0 || c.engine == 5) && (c.inverse_mode == PIT_INV_AUTO || c.inverse_mode == PIT_INV_RECURRENCE) &&
-        law == 1 && c.bc == PIT_PERIODIC && P.nyu % 2 == 0) {
+        (law == 1 ? c.bc == PIT_PERIODIC : true) && P.nyu % 2 == 0) {
         const int dmax = std::max(1, std::min(c.pipeline_depth > 0 ? c.pipeline_depth : 8, c.newton_max));
         for (int D5 = dmax; D5 >= 1 && !h->ps; --D5) {
             for (int Gs = std::min(h->sms / D5, P.nyu / 2); Gs >= 1 && !h->ps; --Gs) {
@@ -515,10 +523,10 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
                 if (he < 2 || na < 0 || na > Gs) continue;
                 size_t smem5 = 0;
                 int thr5 = 0, occ5 = 0, he_used = he;
-                const void* fn = ps_kernel_law1(P.nxu, he, &smem5, &thr5);
+                const void* fn = ps_fn(h, he, &smem5, &thr5);
                 if (!fn && na == 0 && he >= 4) {      // every strip has he rows = (he - 2) + 2
                     he_used = he - 2;
-                    fn = ps_kernel_law1(P.nxu, he_used, &smem5, &thr5);
+                    fn = ps_fn(h, he_used, &smem5, &thr5);
                 }
                 if (!fn || smem5 > 227 * 1024) continue;
                 if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5) != cudaSuccess ||
@@ -763,8 +771,8 @@ static int launch_nb(pit_handle* h, const double* d_u0, const double* ring, doub
 }
 
 // Engine 5: omega and the sweep count as engine 4 (k_nb_q / k_nb_ctl), then the persistent pipeline-of-sets kernel.
-static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double* d_hist, int* d_info, cudaStream_t st,
-                     bool u0_bcast) {
+static int launch_ps(pit_handle* h, const double* d_u0, const double* ring, double* d_u_out, double* d_hist, int* d_info,
+                     cudaStream_t st, bool u0_bcast) {
     NvtxRange nvtx_("engine5 k_newton_ps");
     const Prob& P = h->P;
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
@@ -774,12 +782,12 @@ static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double*
     CUDA_TRY(h, cudaMemsetAsync(h->nb_linres, 0, sizeof(double) * 2 * MAXK, st));
     CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_qbits, 0, sizeof(unsigned long long), st));
-    nb_setup_launch(P, u0_bcast ? d_u0 : h->U, nullptr, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
+    nb_setup_launch(P, u0_bcast ? d_u0 : h->U, ring, h->nb_qbits, h->cfg.lin_rtol, h->cfg.lin_sweeps, h->cfg.lin_check, h->nb_ctl,
                     std::max(1, std::min(grid_for(P.ns, h->sms), 2 * h->sms)), st);
     CUDA_TRY(h, cudaGetLastError());
     PsParams S;
     std::memset(&S, 0, sizeof(S));
-    S.P = P; S.u0 = d_u0; S.U = h->U; S.B = h->B; S.D = h->ps_D; S.Gs = h->ps_Gs;
+    S.P = P; S.u0 = d_u0; S.ring = ring; S.U = h->U; S.B = h->B; S.D = h->ps_D; S.Gs = h->ps_Gs;
     S.ctl = h->nb_ctl; S.llx = h->ps_llx; S.lvl = h->ps_lvl; S.hpart = h->nb_hpart;
     S.arrive = h->nb_sync; S.decided = h->nb_sync + MAXK;
     S.hist = d_hist ? d_hist : h->hist; S.linres = h->nb_linres; S.info = d_info ? d_info : h->info;
@@ -795,7 +803,7 @@ static int launch_ps(pit_handle* h, const double* d_u0, double* d_u_out, double*
     void* args[] = {(void*)&S};
     size_t smem5 = 0;
     int thr5 = 0;
-    const void* fn = ps_kernel_law1(P.nxu, h->ps_he, &smem5, &thr5);
+    const void* fn = ps_fn(h, h->ps_he, &smem5, &thr5);
     CUDA_TRY(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->ps_smem));
     CUDA_TRY(h, cudaLaunchCooperativeKernel(fn, dim3(h->ps_D * h->ps_Gs), dim3(h->ps_threads), args, h->ps_smem, st));
     CUDA_TRY(h, cudaEventRecord(h->ev[3], st));
@@ -1032,7 +1040,7 @@ int pit_solve_device(pit_handle* h, const double* d_u0, const double* d_bc, cons
         CUDA_TRY(h, cudaMemcpyAsync(h->d_u0, d_u0, sizeof(double) * h->P.ns, cudaMemcpyDeviceToDevice, st));
         d_u0 = h->d_u0;
     }
-    if (h->ps) return launch_ps(h, d_u0, d_u_out, d_hist, (int*)d_info, st, ps_bcast);
+    if (h->ps) return launch_ps(h, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_u_out, d_hist, (int*)d_info, st, ps_bcast);
     if (h->nb) return launch_nb(h, d_u0, h->P.bc == PIT_DIRICHLET ? d_bc : nullptr, d_u_out, d_hist, (int*)d_info, st);
     SolveParams S = base_params(h);
     S.u0 = d_u0;
@@ -1113,7 +1121,7 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     if (prod) {
         rc = solve_product(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else if (h->ps) {
-        rc = launch_ps(h, h->d_u0, nullptr, h->hist, h->info, 0, ps_bcast);
+        rc = launch_ps(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0, ps_bcast);
     } else if (h->nb) {
         rc = launch_nb(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else {

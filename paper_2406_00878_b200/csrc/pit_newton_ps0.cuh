@@ -1,66 +1,37 @@
-// pit_newton_ps.cuh — engine 5: the all-at-once Newton solve (Eq. (5)) with the exact block inverse
-// of Eq. (7) applied as the level recurrence du^n = A_n^{-1}(r^n + du^{n-1}), as a PIPELINE OF CTA
-// SETS: set p (Gs CTAs, one per SM) runs Newton iteration k = pass * D + p over the levels n = 1..nt, one level
-// behind set p - 1, so D Newton iterations are in flight on D * Gs SMs (the level wavefront of DESIGN.md §6.1 laid
-// out in space instead of interleaved in every CTA as in engine 4).
-//
-// Per level a CTA holds its strip of H rows (c5: 22 rows of 512) ENTIRELY on chip: du (x) in registers (a thread owns
-// two adjacent columns of one half of the strip's rows: two row groups of NXU / 2 threads), u^n (with its two halo rows)
-// and the right-hand side b = r^n + du^{n-1} in shared memory.  HBM/L2 traffic per (level, iteration): U_k^n read once (into registers, issued before the
-// previous level's epilogue; u^{n-1} is still in shared memory from the previous level) and U_{k+1}^n written once —
-// the 16 B per DOF per Newton iteration of SURVEY §8(d).
-//
-// Level solves: S red-black SOR sweeps from the carry, Young's omega from the Jacobi bound (as engine 4, whose
-// device set-up kernels k_nb_q / k_nb_ctl are reused).  A half-sweep first turns every point of the OTHER colour into
-// its four products with the coefficients its neighbours apply to it (one load of u, seven flops) and scatters them
-// into per-row accumulators, so every value of u and x is touched once per half-sweep.  Synchronisation:
-// neighbouring strips of a set exchange their boundary rows through LL cells (no fences, pit_newton_nb.cuh) once per
-// half-sweep — the loads are issued before the strip's own products and consumed after them, boundary rows are
-// relaxed and published first; set p - 1 hands U_k^n to set p through per-strip level counters (release / acquire)
-// that thread 0 publishes and polls where it would wait for its neighbours anyway.  Columns of neighbouring threads
-// meet through warp shuffles (warp edges through a small shared array).
-//
-// This engine covers LAW 1 (viscous Burgers, constant viscosity) on periodic grids with an even number of rows per
-// strip; everything else runs on engines 1-4.
+// pit_newton_ps0.cuh — engine 5 for the GENERAL LAW (mu(u) = m0 + m2 u^2: the nonlinear heat equation, Burgers with
+// m2 > 0) on Dirichlet or periodic grids: the pipeline of CTA sets of pit_newton_ps.cuh (same schedule, same exchange
+// cells, same level counters, same stop rule; read that file's header first) with the two things the general law
+// changes:
+//  * the coefficients of A_n = I + tau dF/du (Eq. (6)) depend on u at BOTH ends of a face
+//    (mu((u_C + u_nb) / 2) and its derivative, R1), so a neighbour's contribution is not a function of the
+//    neighbour alone: the four off-diagonal coefficients of every own point, divided by its diagonal, are formed once
+//    per level in the residual pass (residual_jacobian_raw, pit_internal.cuh) and kept in shared memory in per-thread
+//    slots (no bank conflicts, no sharing), and a half-sweep GATHERS: x <- (1 - omega) x + omega (b' - sum a' x_nb);
+//  * Dirichlet boundaries (Eq. (2)): strips at the bottom / top of the grid have no neighbouring strip (their halo
+//    row of u comes from the level's boundary ring, the increment du vanishes there), and the first / last column pair
+//    has no x-neighbour thread (its travelling value is a zero slot of the warp-edge array; u from the ring).
+// Rows of 256 unknowns (the coefficient slots of 512-wide strips do not fit in shared memory).
 #pragma once
-#include "pit_newton_nb.cuh"
-#include "pit_ps_params.cuh"
+#include "pit_newton_ps.cuh"
 
 namespace pit {
 
-namespace ps {
-__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
-    unsigned ok;
-    do {
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ unsigned ld_rlx(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-}  // namespace ps
-
-template <int NXU, int HE, int RG>
-struct PsEngine {
-    static_assert(RG == 1 || RG == 2, "one or two row groups");
+template <int NXU, int HE, bool PER>
+struct PsEngine0 {
+    static constexpr int RG = 2;
     static constexpr int T = NXU / 2;          // threads per row group (two columns each)
     static constexpr int NW = T / 32;          // warps per row group
     static constexpr int NTH = RG * T;         // RG = 2: the lower and the upper half of the strip's rows
     static constexpr int HM = HE + 2;          // max strip height (strips have HE or HE + 2 rows, r0 even)
     static constexpr int HHM = HM / RG;        // max rows per thread
-    static constexpr size_t OFF_U = 0;                                    // ubuf [HM + 2][NXU]: u^n rows r0-1 .. r0+H
-    static constexpr size_t OFF_B = OFF_U + (size_t)(HM + 2) * NXU;       // bs   [HHM][2][NTH]
-    static constexpr size_t OFF_A = OFF_B + (size_t)HHM * 2 * NTH;        // acc  [NB_NP][NTH] per-thread norm partials
-    static constexpr size_t OFF_E = OFF_A + (size_t)NB_NP * NTH;          // wedge [RG groups][2 kinds][HHM][NW] warp-edge E/W products
-    static constexpr size_t OFF_G = OFF_E + (size_t)RG * 2 * HHM * NW;    // gx   [2 colours][2][T] N/S products across the row groups
+    static constexpr int UP = NXU + 2;         // ubuf row pitch: [even columns (T)][odd columns (T)][west boundary][east boundary]
+    static constexpr int NWP = NW + 1;         // warp-edge slots per row: one per warp + a zero slot (no x-neighbour: Dirichlet)
+    static constexpr size_t OFF_U = 0;                                    // ubuf [HM + 2][UP]: u^n rows r0-1 .. r0+H
+    static constexpr size_t OFF_B = OFF_U + (size_t)(HM + 2) * UP;        // bs   [HHM][2][NTH] right-hand sides / a_C
+    static constexpr size_t OFF_C = OFF_B + (size_t)HHM * 2 * NTH;        // cf   [4][HHM][2][NTH] a_partner, a_outside, a_N, a_S (each / a_C)
+    static constexpr size_t OFF_A = OFF_C + (size_t)4 * HHM * 2 * NTH;    // acc  [NB_NP][NTH] per-thread norm partials
+    static constexpr size_t OFF_E = OFF_A + (size_t)NB_NP * NTH;          // wedge [RG groups][2 kinds][HHM][NWP] warp-edge values of du
+    static constexpr size_t OFF_G = OFF_E + (size_t)RG * 2 * HHM * NWP;   // gx   [2 colours][2][T] du across the row groups
     static constexpr size_t OFF_R = OFF_G + (size_t)4 * T;                // red  [RG NW][NB_NP]
     static constexpr size_t SMEM = (OFF_R + (size_t)RG * NW * NB_NP) * sizeof(double);
 
@@ -69,18 +40,20 @@ struct PsEngine {
     // column ^ f), so that the colour of local point (q, jj) is (q + jj) & 1 in both groups and every register
     // subscript stays compile-time; the E/W roles then mirror, which only flips the sign of ax and the shuffle
     // direction (per-thread constants).
-    template <int HH, bool ISO>
+    template <int HH>
     __device__ __forceinline__ static void run(const PsParams& S, double* sm) {
         constexpr int H = RG * HH;
         const Prob P = S.P;
         const int Gs = S.Gs, c = blockIdx.x, p = c / Gs, s = c % Gs;
         const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-        const int g = RG == 2 ? tid / T : 0, t = tid % T, wl = w % NW;
+        const int g = tid / T, t = tid % T, wl = w % NW;
         const int nyu = P.nyu, nt = P.nt, D = S.D, B = S.B;
         const long long ns = P.ns;
         const int na = (nyu - HE * Gs) / 2;                 // strips 0 .. na-1 have HE + 2 rows
         const int r0 = s * HE + 2 * min(s, na);             // first row of the strip (even)
-        const int ss = s > 0 ? s - 1 : Gs - 1, sn = s + 1 < Gs ? s + 1 : 0;   // periodic neighbours (rows below / above)
+        // neighbouring strips (rows below / above); -1 = the grid's Dirichlet boundary
+        const int ss = s > 0 ? s - 1 : (PER ? Gs - 1 : -1), sn = s + 1 < Gs ? s + 1 : (PER ? 0 : -1);
+        const int nxp = P.nx + 1;                           // ring layout: bottom [nxp], top [nxp], left [ny-1], right [ny-1]
         const int f = (g * HH) & 1;                         // column swap of this thread (upper group, HH odd)
         const int c0 = 2 * t;
 
@@ -93,10 +66,11 @@ struct PsEngine {
             s_alias = (hint > 0 && hint % B != 0) ? hint % B : -1;
         }
         double* ubuf = sm + OFF_U;
-        double* ub = ubuf + (size_t)(1 + g * HH) * NXU;      // the thread's local row 0 (rows -1 and HH exist too)
+        double* ub = ubuf + (size_t)(1 + g * HH) * UP;       // the thread's local row 0 (rows -1 and HH exist too)
+        double* cfs = sm + OFF_C;
         double* bs = sm + OFF_B;
         double* accs = sm + OFF_A;
-        double* wedge = sm + OFF_E + (size_t)g * 2 * HHM * NW;   // this group's [2 kinds][HHM][NW]
+        double* wedge = sm + OFF_E + (size_t)g * 2 * HHM * NWP;  // this group's [2 kinds][HHM][NWP]
         double* gx0 = sm + OFF_G;                            // per colour: [0][t] lower group's top row -> upper, [1][t] upper's bottom row -> lower
         double* red_s = sm + OFF_R;
         __shared__ int s_dec[2];
@@ -106,8 +80,9 @@ struct PsEngine {
 
         // LL cells of a strip: [ring][side][t]; side 0 = its bottom row (published by the lower group), 1 = its top row
         unsigned long long* myx = S.llx + ((size_t)(p * Gs + s) * PS_RX * 2 * T) * 2;
-        const unsigned long long* sbx = S.llx + ((size_t)(p * Gs + ss) * PS_RX * 2 * T) * 2;   // the strip below
-        const unsigned long long* nbx = S.llx + ((size_t)(p * Gs + sn) * PS_RX * 2 * T) * 2;   // the strip above
+        const unsigned long long* sbx = S.llx + ((size_t)(p * Gs + max(ss, 0)) * PS_RX * 2 * T) * 2;   // the strip below
+        const unsigned long long* nbx = S.llx + ((size_t)(p * Gs + max(sn, 0)) * PS_RX * 2 * T) * 2;   // the strip above
+        const bool has_nb = (g ? sn : ss) >= 0;              // this row group's side of the strip has a neighbouring strip
         auto mycell = [&](unsigned q, int side) { return myx + ((size_t)((q % PS_RX) * 2 + side) * T + t) * 2; };
         auto scell = [&](unsigned q) { return sbx + ((size_t)((q % PS_RX) * 2 + 1) * T + t) * 2; };   // its top row
         auto ncell = [&](unsigned q) { return nbx + ((size_t)((q % PS_RX) * 2 + 0) * T + t) * 2; };   // its bottom row
@@ -115,43 +90,40 @@ struct PsEngine {
         const double omega = __ldcg(S.ctl);
         const int SW = (int)__ldcg(S.ctl + 1);
         const int chk = max(1, (int)__ldcg(S.ctl + 3));
-#define bx (S.bx)
-#define ay (S.ay)
-#define by (S.by)
-#define aC1 (S.aC1)
-#define tau (S.P.dt)
-        const double a1 = f ? -S.ax : S.ax;                  // ax seen through the column swap
-        const double sx2 = f ? -P.i2hx : P.i2hx;             // 1/(2 hx) seen through the column swap (residual)
-        const double oic = omega * S.invC1, om1 = 1.0 - omega;     // x <- om1 x + oic (b - offdiag x)
-        const double rsc = aC1 * (om1 / omega);                      // residual of a just-relaxed point: rsc (x_new - x_old)
+        const double om1 = 1.0 - omega;                      // x <- om1 x + omega (b' - sum a' x_nb), a' = a / a_C
+        const double rsc = om1 / omega;                      // (scaled) residual of a just-relaxed point: rsc (x_new - x_old)
         // kind A rows (other colour in local column 1): the product travels to thread t + 1 (f = 0) or t - 1 (f = 1);
         // kind B rows (other colour in local column 0): the opposite way.
         int srcA = (lane + (f ? 1 : 31)) & 31, srcB = (lane + (f ? 31 : 1)) & 31;
         asm volatile("" : "+r"(srcA), "+r"(srcB));
         const int edgeA = f ? 31 : 0, edgeB = f ? 0 : 31;    // lanes whose source lies in the neighbouring warp
-        const int wsA = f ? (wl + 1) % NW : (wl + NW - 1) % NW, wsB = f ? (wl + NW - 1) % NW : (wl + 1) % NW;
-        double* wdA = wedge;                                 // [HHM][NW]
-        double* wdB = wedge + (size_t)HHM * NW;
+        // the neighbouring warp's slot (periodic: wraps; Dirichlet: the first / last warp's outer side is the zero slot NW)
+        const int wprev = wl > 0 ? wl - 1 : (PER ? NW - 1 : NW), wnext = wl + 1 < NW ? wl + 1 : (PER ? 0 : NW);
+        const int wsA = f ? wnext : wprev, wsB = f ? wprev : wnext;
+        double* wdA = wedge;                                 // [HHM][NWP]
+        double* wdB = wedge + (size_t)HHM * NWP;
         int isA = lane == edgeA, isB = lane == edgeB;         // this lane's kind A / B source lies in the neighbouring warp
         int wrA = lane == 31 - edgeA, wrB = lane == 31 - edgeB;   // this lane's kind A / B product is a neighbouring warp's source
-        unsigned wdA_w = (unsigned)__cvta_generic_to_shared(wdA + wl), wdB_w = (unsigned)__cvta_generic_to_shared(wdB + wl);
+        unsigned wdA_w = (unsigned)__cvta_generic_to_shared(wdA + wl), wdB_w = (unsigned)__cvta_generic_to_shared(wdB + wl);   // rows are NWP apart
         // (opaque to the compiler, which otherwise rebuilds these from the thread index in every row of the sweeps)
         asm volatile("" : "+r"(isA), "+r"(isB), "+r"(wrA), "+r"(wrB), "+r"(wdA_w), "+r"(wdB_w));
         // ubuf rows are de-interleaved: [even columns (T)][odd columns (T)], so that a warp's loads of one local column
         // are contiguous (no bank conflicts).  Offsets of local columns 0 and 1, and of their out-of-thread x-neighbours
         // (actual column c0 - 1: odd, pair t - 1; actual column c0 + 2: even, pair t + 1; periodic).
         const int uo0 = f * T + t, uo1 = (1 - f) * T + t;
-        const int cwest = T + (t + T - 1) % T, ceast = (t + 1) % T;
+        const int cwest = t > 0 ? T + t - 1 : (PER ? 2 * T - 1 : NXU), ceast = t + 1 < T ? t + 1 : (PER ? 0 : NXU + 1);
         const int co0 = f ? ceast : cwest, co1 = f ? cwest : ceast;
 
         auto cbar = [&]() { __syncthreads(); };
         auto bsm = [&](int r, int j) -> double& { return bs[(size_t)(r * 2 + j) * NTH + tid]; };
+        auto cfm = [&](int kind, int r, int j) -> double& { return cfs[(size_t)((kind * HHM + r) * 2 + j) * NTH + tid]; };   // 0 partner, 1 outside, 2 N, 3 S
         auto ac = [&](int j) -> double& { return accs[(size_t)j * NTH + tid]; };
         auto lswap = [&](double2 v) { return f ? make_double2(v.y, v.x) : v; };   // actual <-> local column order
 
         double x[HH][2];
         #pragma unroll
         for (int j = 0; j < NB_NP; ++j) ac(j) = 0.0;
+        for (int i = tid; i < RG * 2 * HHM * NWP; i += NTH) (sm + OFF_E)[i] = 0.0;   // (the zero slots stay zero: nobody writes them)
         int lastx = -1;
         unsigned qx = 0;
         int levels = 0;
@@ -182,7 +154,11 @@ struct PsEngine {
         // CTA's loads of their rows (which follow the next CTA barrier).
         auto service = [&](unsigned base) {
             unsigned v0 = 0xffffffffu, v1 = 0xffffffffu, v2 = 0xffffffffu;
-            if (pf_lv && fprev) { v0 = ps::ld_rlx(fprev + s); v1 = ps::ld_rlx(fprev + ss); v2 = ps::ld_rlx(fprev + sn); }
+            if (pf_lv && fprev) {
+                v0 = ps::ld_rlx(fprev + s);
+                if (ss >= 0) v1 = ps::ld_rlx(fprev + ss);
+                if (sn >= 0) v2 = ps::ld_rlx(fprev + sn);
+            }
             const bool ready = pf_lv && min(v0, min(v1, v2)) >= base + (unsigned)pf_lv;
             if ((flag_lv || (ready && fprev)) && !(S.dbg & 2)) __threadfence();   // (dbg bit 1: timing experiment without the fence)
             if (flag_lv) {
@@ -192,93 +168,59 @@ struct PsEngine {
             if (ready) pf_lv = 0;
         };
 
-        // tt[q] = b - (off-diagonal part of A_n) x at the colour-cc point of every own row q (local column (q + cc) & 1).
-        // Every point of the other colour is turned into its products with the coefficients its four neighbours apply
-        // to it: a_E = ax u - bx (seen from its W neighbour), a_W = -ax u - bx, a_N = ay u - by (seen from the row
-        // below), a_S = -ay u - by.  The product for the neighbouring THREAD travels by warp shuffle (warp edges through
-        // shared memory), the one for the other row group through shared memory, and the neighbouring strip's row
-        // arrives in an LL cell.
+        // tt[q] = b' - sum a' x_nb at the colour-cc point of every own row q (local column j = (q + cc) & 1), with the
+        // point's own coefficients a' = a / a_C from its shared-memory slots.  Its x-neighbour inside the thread is the
+        // other column of the row, the one outside travels by warp shuffle (warp edges through shared memory, the
+        // grid's edge through the zero slot), the rows above / below are the thread's own registers, the other row
+        // group's boundary row (shared memory) or the neighbouring strip's (LL cell; none at a Dirichlet boundary).
         auto gather = [&](const int cc, double (&tt)[HH], const bool svc, const unsigned fbase) {
-            LLc hcs, hcn;                                    // RG = 2: a thread has one neighbouring strip (hcs holds its cell)
+            LLc hc;
             const unsigned qn = (unsigned)lastx;
-            if (lastx >= 0) {
-                if constexpr (RG == 1) {
-                    hcs = ll_issue(scell(qn));
-                    hcn = ll_issue(ncell(qn));
-                } else {
-                    hcs = ll_issue(g ? ncell(qn) : scell(qn));
-                }
-            }
+            const bool ll = lastx >= 0 && has_nb;
+            if (ll) hc = ll_issue(g ? ncell(qn) : scell(qn));
             if (svc && tid == 0 && (flag_lv | pf_lv)) service(fbase);
             double* gx = gx0 + (size_t)cc * 2 * T;           // double-buffered: a fast warp's next half-sweep writes the other half
             #pragma unroll
-            for (int q = 0; q < HH; ++q) tt[q] = bsm(q, (q + cc) & 1);
-            #pragma unroll
             for (int q = 0; q < HH; ++q) {
-                const int jn = 1 - ((q + cc) & 1);               // the other colour's local column in this row
-                const double uq = ub[(size_t)q * NXU + (jn ? uo1 : uo0)], xq = x[q][jn];
-                // (a1 u - bx) x and (-a1 u - bx) x = -(a1 u - bx) x - 2 bx x; the same in y (on an isotropic grid the y
-                // products ARE the x products: the +a form is pa unless the columns are swapped)
-                const double pa = fma(a1, uq, -bx) * xq, pb = fma(-2.0 * bx, xq, -pa);
-                double pn, psv;
-                if (ISO) {
-                    pn = f ? pb : pa;
-                    psv = f ? pa : pb;
+                const int j = (q + cc) & 1, jn = 1 - j;
+                const double xq = x[q][jn];                   // this row's point of the other colour
+                double acc = fma(-cfm(0, q, j), xq, bsm(q, j));
+                if (jn == 1) {               // kind A: the value travels as for the constant-viscosity law
+                    const double in = __shfl_sync(0xffffffffu, xq, srcA);
+                    if (!isA) acc = fma(-cfm(1, q, j), in, acc);
+                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
+                                 ::"r"(wdA_w + (unsigned)(q * NWP * 8)), "d"(xq), "r"(wrA) : "memory");
                 } else {
-                    pn = fma(ay, uq, -by) * xq;
-                    psv = fma(-2.0 * by, xq, -pn);
-                }
-                // the travelling product goes to the neighbouring thread at once (shuffle); the lanes whose source lies in
-                // the neighbouring warp take theirs from shared memory behind the barrier instead
-                if (jn == 1) {               // kind A: in-thread term pa, travelling term pb
-                    const double in = __shfl_sync(0xffffffffu, pb, srcA);
-                    tt[q] -= pa;
-                    if (!isA) tt[q] -= in;
+                    const double in = __shfl_sync(0xffffffffu, xq, srcB);
+                    if (!isB) acc = fma(-cfm(1, q, j), in, acc);
                     asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
-                                 ::"r"(wdA_w + (unsigned)(q * NW * 8)), "d"(pb), "r"(wrA) : "memory");
-                } else {                     // kind B: in-thread term pb, travelling term pa
-                    const double in = __shfl_sync(0xffffffffu, pa, srcB);
-                    tt[q] -= pb;
-                    if (!isB) tt[q] -= in;
-                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
-                                 ::"r"(wdB_w + (unsigned)(q * NW * 8)), "d"(pa), "r"(wrB) : "memory");
+                                 ::"r"(wdB_w + (unsigned)(q * NWP * 8)), "d"(xq), "r"(wrB) : "memory");
                 }
-                if (q > 0) tt[q > 0 ? q - 1 : 0] -= pn;
-                else if (RG == 2 && g == 1) gx[T + t] = pn;  // to the lower group's top row
-                if (q + 1 < HH) tt[q + 1 < HH ? q + 1 : q] -= psv;
-                else if (RG == 2 && g == 0) gx[t] = psv;     // to the upper group's bottom row
+                if (q + 1 < HH) acc = fma(-cfm(2, q, j), x[q + 1 < HH ? q + 1 : q][j], acc);
+                if (q > 0) acc = fma(-cfm(3, q, j), x[q > 0 ? q - 1 : 0][j], acc);
+                tt[q] = acc;
             }
+            // this group's boundary row towards the other group: its point of the other colour (raw du)
+            if (g == 0) gx[t] = x[HH - 1][1 - ((HH - 1 + cc) & 1)];
+            else gx[T + t] = x[0][1 - (cc & 1)];
             cbar();
             if (isA) {
                 #pragma unroll
                 for (int q = 0; q < HH; ++q)
-                    if ((q + cc) & 1) {} else tt[q] -= wdA[q * NW + wsA];      // kind A rows: other colour in local column 1
+                    if (((q + cc) & 1) == 0) tt[q] = fma(-cfm(1, q, 0), wdA[q * NWP + wsA], tt[q]);      // kind A rows: active column 0
             }
             if (isB) {
                 #pragma unroll
                 for (int q = 0; q < HH; ++q)
-                    if ((q + cc) & 1) tt[q] -= wdB[q * NW + wsB];              // kind B rows
+                    if ((q + cc) & 1) tt[q] = fma(-cfm(1, q, 1), wdB[q * NWP + wsB], tt[q]);             // kind B rows: active column 1
             }
             // the row below local row 0 and the row above local row HH-1: the other row group or the neighbouring strip
-            if (RG == 2) {
-                if (g == 0) tt[HH - 1] -= gx[T + t]; else tt[0] -= gx[t];
-            }
-            if (lastx >= 0) {
-                if constexpr (RG == 1) {
-                    const double xs = take(scell(qn), hcs, qn + 1u), xn = take(ncell(qn), hcn, qn + 1u);
-                    const double us = ub[-(ptrdiff_t)NXU + ((cc & 1) ? uo1 : uo0)];
-                    const double un = ub[(size_t)HH * NXU + (((HH - 1 + cc) & 1) ? uo1 : uo0)];
-                    tt[0] = fma(-fma(-ay, us, -by), xs, tt[0]);
-                    tt[HH - 1] = fma(-fma(ay, un, -by), xn, tt[HH - 1]);
-                } else if (g == 0) {
-                    const double xh = take(scell(qn), hcs, qn + 1u);
-                    const double uh = ub[-(ptrdiff_t)NXU + ((cc & 1) ? uo1 : uo0)];
-                    tt[0] = fma(-fma(-ay, uh, -by), xh, tt[0]);
-                } else {
-                    const double xh = take(ncell(qn), hcs, qn + 1u);
-                    const double uh = ub[(size_t)HH * NXU + (((HH - 1 + cc) & 1) ? uo1 : uo0)];
-                    tt[HH - 1] = fma(-fma(ay, uh, -by), xh, tt[HH - 1]);
-                }
+            if (g == 0) {
+                tt[HH - 1] = fma(-cfm(2, HH - 1, (HH - 1 + cc) & 1), gx[T + t], tt[HH - 1]);
+                if (ll) tt[0] = fma(-cfm(3, 0, cc & 1), take(scell(qn), hc, qn + 1u), tt[0]);
+            } else {
+                tt[0] = fma(-cfm(3, 0, cc & 1), gx[t], tt[0]);
+                if (ll) tt[HH - 1] = fma(-cfm(2, HH - 1, (HH - 1 + cc) & 1), take(ncell(qn), hc, qn + 1u), tt[HH - 1]);
             }
         };
 
@@ -295,8 +237,8 @@ struct PsEngine {
                 for (int r = 0; r < HH; ++r) {
                     x[r][0] = 0.0; x[r][1] = 0.0;
                     const double2 v = ldcg2(S.u0 + (size_t)(rg0 + r) * NXU + c0);     // u^{n-1} of level 1
-                    ub[(size_t)r * NXU + t] = v.x;
-                    ub[(size_t)r * NXU + T + t] = v.y;
+                    ub[(size_t)r * UP + t] = v.x;
+                    ub[(size_t)r * UP + T + t] = v.y;
                 }
                 lastx = -1;
                 if (tid == 0) pf_lv = 1;
@@ -316,56 +258,63 @@ struct PsEngine {
                 // ---- prologue 1: b = du^{n-1} - (u^n - u^{n-1}); u^n replaces u^{n-1} in shared memory
                 {
                     const double* un = (k == 0 && S.u0_bcast) ? S.u0 + c0 : ring_buf(S, s_alias, k % B) + (size_t)(n - 1) * ns + c0;
-                    double2 pf[HH + RG % 2 + 1];                    // own rows, then the strip's halo row(s) this thread stores
+                    const double* rgn = (!PER && S.ring) ? S.ring + (size_t)(n - 1) * P.ring_len : nullptr;   // level n's boundary ring
+                    double2 pf[HH + 1];                             // own rows, then this group's strip-halo row
                     #pragma unroll
                     for (int r = 0; r < HH; ++r) pf[r] = ldcg2(un + (size_t)(rg0 + r) * NXU);
-                    if constexpr (RG == 1) {
-                        pf[HH] = ldcg2(un + (size_t)((rg0 - 1 + nyu) % nyu) * NXU);
-                        pf[HH + 1] = ldcg2(un + (size_t)((rg0 + HH) % nyu) * NXU);
-                    } else {
+                    if (has_nb) {
                         pf[HH] = ldcg2(un + (size_t)(g ? (rg0 + HH) % nyu : (rg0 - 1 + nyu) % nyu) * NXU);
+                    } else {                                        // Dirichlet: the ring's bottom (j = 0) / top (j = ny) row, i = c0 + 1, c0 + 2
+                        const double* rr = rgn ? rgn + (g ? nxp : 0) + c0 + 1 : nullptr;
+                        pf[HH] = rr ? make_double2(__ldcg(rr), __ldcg(rr + 1)) : make_double2(0.0, 0.0);
                     }
                     #pragma unroll
                     for (int r = 0; r < HH; ++r) {
                         const double2 nw = lswap(pf[r]);
-                        bsm(r, 0) = x[r][0] - (nw.x - ub[(size_t)r * NXU + uo0]);
-                        bsm(r, 1) = x[r][1] - (nw.y - ub[(size_t)r * NXU + uo1]);
-                        ub[(size_t)r * NXU + t] = pf[r].x;
-                        ub[(size_t)r * NXU + T + t] = pf[r].y;
+                        bsm(r, 0) = x[r][0] - (nw.x - ub[(size_t)r * UP + uo0]);
+                        bsm(r, 1) = x[r][1] - (nw.y - ub[(size_t)r * UP + uo1]);
+                        ub[(size_t)r * UP + t] = pf[r].x;
+                        ub[(size_t)r * UP + T + t] = pf[r].y;
                     }
-                    if constexpr (RG == 1) {
-                        ub[-(ptrdiff_t)NXU + t] = pf[HH].x;
-                        ub[-(ptrdiff_t)NXU + T + t] = pf[HH].y;
-                        ub[(size_t)HH * NXU + t] = pf[HH + 1].x;
-                        ub[(size_t)HH * NXU + T + t] = pf[HH + 1].y;
-                    } else {
-                        double* hrow = g ? ub + (size_t)HH * NXU : ub - (ptrdiff_t)NXU;
-                        hrow[t] = pf[HH].x;
-                        hrow[T + t] = pf[HH].y;
+                    double* hrow = g ? ub + (size_t)HH * UP : ub - (ptrdiff_t)UP;
+                    hrow[t] = pf[HH].x;
+                    hrow[T + t] = pf[HH].y;
+                    if (!PER && (t == 0 || t == T - 1)) {           // the level's left / right boundary values of the own rows
+                        #pragma unroll
+                        for (int r = 0; r < HH; ++r) {
+                            const int jr = rg0 + r;
+                            if (t == 0) ub[(size_t)r * UP + NXU] = rgn ? __ldcg(rgn + 2 * nxp + jr) : 0.0;
+                            if (t == T - 1) ub[(size_t)r * UP + NXU + 1] = rgn ? __ldcg(rgn + 2 * nxp + (P.ny - 1) + jr) : 0.0;
+                        }
                     }
                 }
                 cbar();
                 if (tid == 0 && n < nt) pf_lv = n + 1;
                 mark(0);
-                // ---- prologue 2: r^n = -G^n, b = r^n + du^{n-1} (local column order: the x-differences carry sx2)
+                // ---- prologue 2: r^n = -G^n, b = r^n + du^{n-1}, and the rows of A_n (Eq. (6)), everything divided by a_C
                 {
                     double ar2 = 0.0, arm = 0.0;
-                    double p0 = ub[-(ptrdiff_t)NXU + uo0], p1 = ub[-(ptrdiff_t)NXU + uo1];
+                    double p0 = ub[-(ptrdiff_t)UP + uo0], p1 = ub[-(ptrdiff_t)UP + uo1];
                     double c0v = ub[uo0], c1v = ub[uo1];
                     #pragma unroll
                     for (int r = 0; r < HH; ++r) {
-                        const double n0 = ub[(size_t)(r + 1) * NXU + uo0], n1 = ub[(size_t)(r + 1) * NXU + uo1];
-                        const double o0 = ub[(size_t)r * NXU + co0], o1 = ub[(size_t)r * NXU + co1];
-                        // local column 0: x-neighbours o0 (outside) and c1v; local column 1: c0v and o1 (outside)
-                        const double conv0 = 0.5 * ((c1v * c1v - o0 * o0) * sx2 + (n0 * n0 - p0 * p0) * P.i2hy);
-                        const double visc0 = P.m0 * ((c1v - 2.0 * c0v + o0) * P.ihx2 + (n0 - 2.0 * c0v + p0) * P.ihy2);
-                        const double conv1 = 0.5 * ((o1 * o1 - c0v * c0v) * sx2 + (n1 * n1 - p1 * p1) * P.i2hy);
-                        const double visc1 = P.m0 * ((o1 - 2.0 * c1v + c0v) * P.ihx2 + (n1 - 2.0 * c1v + p1) * P.ihy2);
-                        const double f0 = tau * (conv0 - visc0), f1 = tau * (conv1 - visc1);
+                        const double n0 = ub[(size_t)(r + 1) * UP + uo0], n1 = ub[(size_t)(r + 1) * UP + uo1];
+                        const double o0 = ub[(size_t)r * UP + co0], o1 = ub[(size_t)r * UP + co1];
+                        // local column 0 is actual column f: its outside x-neighbour is W (f = 0) or E (f = 1), the partner the other
+                        Vals v0, v1;
+                        v0.c = c0v; v0.n = n0; v0.s = p0; v0.e = f ? o0 : c1v; v0.w = f ? c1v : o0;
+                        v1.c = c1v; v1.n = n1; v1.s = p1; v1.e = f ? c0v : o1; v1.w = f ? o1 : c0v;
+                        const RJ j0 = residual_jacobian_raw(P, v0, 0.0), j1 = residual_jacobian_raw(P, v1, 0.0);
+                        const double f0 = j0.G - c0v, f1 = j1.G - c1v;                          // tau F(u^n)
                         const double b0 = bsm(r, 0), b1 = bsm(r, 1);
                         const double G0 = (x[r][0] - b0) + f0, G1 = (x[r][1] - b1) + f1;     // (u^n - u^{n-1}) + tau F(u^n)
-                        bsm(r, 0) = b0 - f0;
-                        bsm(r, 1) = b1 - f1;
+                        const double i0 = 1.0 / j0.aC, i1 = 1.0 / j1.aC;
+                        bsm(r, 0) = (b0 - f0) * i0;
+                        bsm(r, 1) = (b1 - f1) * i1;
+                        cfm(0, r, 0) = (f ? j0.aW : j0.aE) * i0;  cfm(1, r, 0) = (f ? j0.aE : j0.aW) * i0;
+                        cfm(2, r, 0) = j0.aN * i0;                cfm(3, r, 0) = j0.aS * i0;
+                        cfm(0, r, 1) = (f ? j1.aE : j1.aW) * i1;  cfm(1, r, 1) = (f ? j1.aW : j1.aE) * i1;
+                        cfm(2, r, 1) = j1.aN * i1;                cfm(3, r, 1) = j1.aS * i1;
                         ar2 = fma(G0, G0, fma(G1, G1, ar2));
                         arm = fmax(arm, fmax(fabs(G0), fabs(G1)));
                         p0 = c0v; p1 = c1v; c0v = n0; c1v = n1;
@@ -387,18 +336,13 @@ struct PsEngine {
                             #pragma unroll
                             for (int r = 0; r < HH; ++r) {
                                 const int j = (r + cc) & 1;
-                                const double xo = x[r][j], xn = fma(oic, tt[r], om1 * xo);
+                                const double xo = x[r][j], xn = fma(omega, tt[r], om1 * xo);
                                 x[r][j] = xn;
                                 const double rr = rsc * (xn - xo);
                                 rs2 = fma(rr, rr, rs2);
                                 rsm = fmax(rsm, fabs(rr));
                             }
-                            if constexpr (RG == 1) {
-                                ll_put(mycell(qx, 0), x[0][cc & 1], qx + 1u);
-                                ll_put(mycell(qx, 1), x[HH - 1][(HH - 1 + cc) & 1], qx + 1u);
-                            } else {
-                                ll_put(mycell(qx, g), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
-                            }
+                            if (has_nb) ll_put(mycell(qx, g), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
                             ac(4) += rs2;
                             ac(5) = fmax(ac(5), rsm);
                         } else {
@@ -407,14 +351,9 @@ struct PsEngine {
                                 const int r = i == 0 ? 0 : (i == 1 ? HH - 1 : i - 1);     // the two end rows first: one of them is the strip's boundary row
                                 const int j = (r + cc) & 1;
                                 const double xo = x[r][j];
-                                x[r][j] = fma(oic, tt[r], om1 * xo);
+                                x[r][j] = fma(omega, tt[r], om1 * xo);
                                 if (i == (HH > 1 ? 1 : 0)) {     // publish the strip's boundary rows: local row 0 of the lower group, HH-1 of the upper
-                                    if constexpr (RG == 1) {
-                                        ll_put(mycell(qx, 0), x[0][cc & 1], qx + 1u);
-                                        ll_put(mycell(qx, 1), x[HH - 1][(HH - 1 + cc) & 1], qx + 1u);
-                                    } else {
-                                        ll_put(mycell(qx, g), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
-                                    }
+                                    if (has_nb) ll_put(mycell(qx, g), g ? x[HH - 1][(HH - 1 + cc) & 1] : x[0][cc & 1], qx + 1u);
                                 }
                             }
                         }
@@ -430,8 +369,8 @@ struct PsEngine {
                     #pragma unroll
                     for (int r = 0; r < HH; ++r) {
                         double2 v;
-                        v.x = ub[(size_t)r * NXU + uo0] + x[r][0];
-                        v.y = ub[(size_t)r * NXU + uo1] + x[r][1];
+                        v.x = ub[(size_t)r * UP + uo0] + x[r][0];
+                        v.y = ub[(size_t)r * UP + uo1] + x[r][1];
                         *reinterpret_cast<double2*>(Un + (size_t)(rg0 + r) * NXU + c0) = lswap(v);
                         d2 = fma(x[r][0], x[r][0], fma(x[r][1], x[r][1], d2));
                         dm = fmax(dm, fmax(fabs(x[r][0]), fabs(x[r][1])));
@@ -448,7 +387,7 @@ struct PsEngine {
                     double rs2 = 0.0, rsm = 0.0, bb2 = 0.0;
                     #pragma unroll
                     for (int r = 0; r < HH; ++r) {
-                        const double rr = tt[r] - aC1 * x[r][r & 1];
+                        const double rr = tt[r] - x[r][r & 1];
                         rs2 = fma(rr, rr, rs2);
                         rsm = fmax(rsm, fabs(rr));
                         bb2 = fma(bsm(r, 0), bsm(r, 0), fma(bsm(r, 1), bsm(r, 1), bb2));
@@ -578,46 +517,31 @@ struct PsEngine {
         }
         if (c == 0 && tid == 0) *S.hint = s_dec[1];         // the next solve keeps that ring slot in its u_out
         copy_out(S, s_alias, s_dec[1]);
-#undef bx
-#undef ay
-#undef by
-#undef aC1
-#undef tau
     }
 
     // The converged iterate (buffer kf % B) copied to u_out by every CTA of the grid.
-    // Ring buffer i of the iterate ring; slot `alias` (if any) is the caller's u_out.
     __device__ __forceinline__ static double* ring_buf(const PsParams& S, int alias, int i) {
         return i == alias ? S.u_out : S.U + (size_t)i * S.P.nt * S.P.ns;
     }
+    // The converged iterate (buffer kf % B) copied to u_out by every CTA of the grid (unless it was written in place).
     __device__ __forceinline__ static void copy_out(const PsParams& S, int alias, int kf) {
-        if (!S.u_out || kf % S.B == alias) return;        // the final iterate was written in place
+        if (!S.u_out || kf % S.B == alias) return;
         const long long n2 = (long long)S.P.nt * S.P.ns / 2;
         const double2* src = reinterpret_cast<const double2*>(ring_buf(S, alias, kf % S.B));
         double2* dst = reinterpret_cast<double2*>(S.u_out);
         const long long stride = (long long)S.D * S.Gs * NTH;
-        long long i = (long long)blockIdx.x * NTH + threadIdx.x;
-        for (; i + 3 * stride < n2; i += 4 * stride) {
-            const double2 a = __ldcg(src + i), b = __ldcg(src + i + stride), cc = __ldcg(src + i + 2 * stride), d = __ldcg(src + i + 3 * stride);
-            __stcs(dst + i, a); __stcs(dst + i + stride, b); __stcs(dst + i + 2 * stride, cc); __stcs(dst + i + 3 * stride, d);
-        }
-        for (; i < n2; i += stride) __stcs(dst + i, __ldcg(src + i));
+        for (long long i = (long long)blockIdx.x * NTH + threadIdx.x; i < n2; i += stride) __stcs(dst + i, __ldcg(src + i));
     }
 };
 
-template <int NXU, int HE, int RG>
-__global__ void __launch_bounds__(RG * NXU / 2, 1) k_newton_ps(const PsParams S) {
-    extern __shared__ __align__(128) double sm_ps[];
-    using E = PsEngine<NXU, HE, RG>;
+template <int NXU, int HE, bool PER>
+__global__ void __launch_bounds__(NXU, 1) k_newton_ps0(const PsParams S) {
+    extern __shared__ __align__(128) double sm_ps0[];
+    using E = PsEngine0<NXU, HE, PER>;
     if ((int)blockIdx.x >= S.D * S.Gs) return;
     const int s = blockIdx.x % S.Gs;
     const int na = (S.P.nyu - HE * S.Gs) / 2;
-    const bool iso = S.ax == S.ay && S.bx == S.by;      // hx = hy: the y products of the sweeps are the x products
-    if (s < na) {
-        if (iso) E::template run<(HE + 2) / RG, true>(S, sm_ps); else E::template run<(HE + 2) / RG, false>(S, sm_ps);
-    } else {
-        if (iso) E::template run<HE / RG, true>(S, sm_ps); else E::template run<HE / RG, false>(S, sm_ps);
-    }
+    if (s < na) E::template run<(HE + 2) / 2>(S, sm_ps0); else E::template run<HE / 2>(S, sm_ps0);
 }
 
 }  // namespace pit

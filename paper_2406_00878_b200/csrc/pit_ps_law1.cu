@@ -4,17 +4,19 @@
 
 namespace pit {
 
-template <int NXU, int HE>
+template <int NXU, int HE, int RG>
 static const void* ps_inst(size_t* smem, int* threads) {
-    *smem = PsEngine<NXU, HE>::SMEM;
-    *threads = PsEngine<NXU, HE>::NTH;
-    return (const void*)k_newton_ps<NXU, HE>;
+    *smem = PsEngine<NXU, HE, RG>::SMEM;
+    *threads = PsEngine<NXU, HE, RG>::NTH;
+    return (const void*)k_newton_ps<NXU, HE, RG>;
 }
 
 // Instantiated shapes: (row length, base strip height HE); a set's strips have HE or HE + 2 rows.
-const void* ps_kernel_law1(int nxu, int he, size_t* smem, int* threads) {
-    if (nxu == 512 && he == 20) return ps_inst<512, 20>(smem, threads);     // BASELINE c5: 6 sets of 24 strips
-    if (nxu == 256 && he == 14) return ps_inst<256, 14>(smem, threads);     // BASELINE c4: 8 sets of 18 strips
+const void* ps_kernel_law1(int nxu, int he, int rg, size_t* smem, int* threads) {
+    if (nxu == 512 && he == 20 && rg == 1) return ps_inst<512, 20, 1>(smem, threads);   // (experiment: one row group, 256 threads)
+    if (rg != 2) return nullptr;
+    if (nxu == 512 && he == 20) return ps_inst<512, 20, 2>(smem, threads);     // BASELINE c5: 6 sets of 24 strips
+    if (nxu == 256 && he == 14) return ps_inst<256, 14, 2>(smem, threads);     // BASELINE c4: 8 sets of 18 strips
     return nullptr;
 }
 

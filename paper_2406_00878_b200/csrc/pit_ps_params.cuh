@@ -11,6 +11,7 @@ constexpr int PS_TR = 8;     // trace: stage wait, prologue, sweeps, LL waits, e
 struct PsParams {
     Prob P;
     const double* u0;           // [ns], 16-byte aligned
+    const double* ring;         // [nt][ring_len] Dirichlet boundary values per level, or nullptr (homogeneous / periodic)
     double* U;                  // [B][nt][ns] iterate ring (iterate k in buffer k % B), buffer 0 = U_0
     int B, D, Gs;               // ring buffers (>= D + 1), CTA sets (iterations in flight), strips per set
     const double* ctl;          // [4] = { omega, sweeps, q, check stride } (k_nb_ctl)
@@ -36,7 +37,9 @@ struct PsParams {
 };
 
 // Implemented in pit_ps_law1.cu: the engine-5 kernel for (row length, base strip height), its dynamic shared memory
-// and threads; nullptr if that shape has no instantiation.
-const void* ps_kernel_law1(int nxu, int he, size_t* smem, int* threads);
+// and threads; rg = row groups per CTA (2; 1 = the 256-thread experiment); nullptr if that shape has no instantiation.
+const void* ps_kernel_law1(int nxu, int he, int rg, size_t* smem, int* threads);
+// Implemented in pit_ps_law0.cu (pit_newton_ps0.cuh): the general law, Dirichlet or periodic.
+const void* ps_kernel_law0(int nxu, int he, int periodic, size_t* smem, int* threads);
 
 }  // namespace pit

@@ -97,7 +97,9 @@ def test_engine5_is_the_default_where_it_applies():
     U, hist, nit, st, stats = gpu_solve(q)
     assert stats["engine"] == 4 and st in (0, 1)
     with pytest.raises(pit.PitError):
-        pit.Solver(W.config(3, nt=2), engine=5)     # heat law, Dirichlet: not covered
+        pit.Solver(W.config(1), engine=5)           # 16 unknowns per row: not covered
+    U, hist, nit, st, stats = gpu_solve(W.config(3, nt=2))
+    assert stats["engine"] == 5 and st in (0, 1)    # the general law on a Dirichlet grid, 256 unknowns per row
 
 
 def test_engine5_level_residuals_and_history_rows():
@@ -169,3 +171,40 @@ def test_engine5_repeated_solves_on_one_handle():
         assert i4[1] in (0, 1) and i4[0] <= 2 and normwise_rel(U4, U1) <= 1e-12
     finally:
         s.close()
+
+
+# ---- the general law (nonlinear heat) on Dirichlet and periodic grids: pit_newton_ps0.cuh ----------------------------
+def _heat(nxu, nyu, nt, bc, dt=5e-4, ring_fn=None, seed=1):
+    rng = np.random.default_rng(seed)
+    if bc == W.DIRICHLET:
+        p = W.custom(f"heat_dir_{nxu}x{nyu}x{nt}", W.HEAT, W.DIRICHLET, nxu + 1, nyu + 1, nt, dt, 1.0, 1.0, u0=np.zeros(nxu * nyu))
+    else:
+        p = W.custom(f"heat_per_{nxu}x{nyu}x{nt}", W.HEAT, W.PERIODIC, nxu, nyu, nt, dt, 1.0, 1.0, u0=np.zeros(nxu * nyu))
+    X, Y = p.grid()
+    base = np.sin(np.pi * X) * np.sin(2 * np.pi * Y) + 0.3 * np.cos(2 * np.pi * X) * np.sin(np.pi * Y)
+    p.u0 = np.ascontiguousarray((base + 1e-3 * rng.standard_normal(X.shape)).reshape(-1))
+    if ring_fn is not None:
+        p.ring = W.ring_from(p, ring_fn)
+    return p
+
+
+HEAT_CASES = [
+    # Dirichlet: 24 rows = 12 + 12 (two strips), 44 = 12 + 12 + 10 + 10, homogeneous and time-dependent rings
+    ("heat_dir_256x24x4_d2", lambda: _heat(256, 24, 4, W.DIRICHLET), 2),
+    ("heat_dir_256x44x5_d3", lambda: _heat(256, 44, 5, W.DIRICHLET), 3),
+    ("heat_dir_ring_256x44x4_d2", lambda: _heat(256, 44, 4, W.DIRICHLET, ring_fn=lambda x, y, t: 0.2 * np.cos(3 * x + 2 * y) * (1 + 5 * t)), 2),
+    ("heat_per_256x44x4_d2", lambda: _heat(256, 44, 4, W.PERIODIC), 2),
+    ("c3_prefix", lambda: W.config(3, nt=3), 0),
+]
+
+
+@pytest.mark.parametrize("name,make,depth", HEAT_CASES, ids=[c[0] for c in HEAT_CASES])
+def test_engine5_general_law_matches_oracle(name, make, depth):
+    p = make()
+    U, hist, nit, st, stats = _sol(p, pipeline_depth=depth)
+    assert st in (pit.PIT_OK, pit.PIT_OK_FLOOR), (st, hist)
+    seq = O.solve_sequential(p)
+    assert seq.status == 0
+    assert normwise_rel(U, seq.U) <= 1e-10, normwise_rel(U, seq.U)
+    U4, h4, n4, s4, st4 = gpu_solve(p, engine=4)
+    assert st4["engine"] == 4 and n4 == nit and normwise_rel(U, U4) <= 1e-12
