@@ -17,6 +17,7 @@ const void* ps_kernel_law1(int nxu, int he, int rg, size_t* smem, int* threads) 
     if (rg != 2) return nullptr;
     if (nxu == 512 && he == 20) return ps_inst<512, 20, 2>(smem, threads);     // BASELINE c5: 6 sets of 24 strips
     if (nxu == 256 && he == 14) return ps_inst<256, 14, 2>(smem, threads);     // BASELINE c4: 8 sets of 18 strips
+    if (nxu == 64 && he == 2) return ps_inst<64, 2, 2>(smem, threads);         // BASELINE c2: 8 sets of 18 strips of 4 / 2 rows
     return nullptr;
 }
 

@@ -47,6 +47,7 @@ CASES = [
     ("burgers_256x44x7_d4", lambda: _burgers(256, 44, 7, dt=2e-4), 4),
     ("c5_prefix", lambda: W.config(5, nt=8), 0),
     ("c4_prefix", lambda: W.config(4, nt=12), 0),
+    ("c2_full", lambda: W.config(2), 0),                       # 64 unknowns per row: one warp per row group, strips of 4 / 2 rows
 ]
 
 
@@ -93,7 +94,7 @@ def test_engine5_is_the_default_where_it_applies():
     p = W.config(5, nt=4)
     U, hist, nit, st, stats = gpu_solve(p)
     assert stats["engine"] == 5 and st in (0, 1)
-    q = W.config(2)                       # 64 unknowns per row: no engine-5 instantiation, engine 4 takes it
+    q = W.config(2, n=128, nt=4)          # 128 unknowns per row: no engine-5 instantiation, engine 4 takes it
     U, hist, nit, st, stats = gpu_solve(q)
     assert stats["engine"] == 4 and st in (0, 1)
     with pytest.raises(pit.PitError):

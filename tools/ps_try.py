@@ -69,6 +69,10 @@ if __name__ == "__main__":
             print("c5 nt=64 engine 5 vs 4:", normwise_rel(U5, U4))
         elif a == "c4":
             timed(4, engine=5)
+        elif a == "c2":
+            U5 = timed(2, engine=5)
+            U4 = timed(2, engine=4)
+            print("c2 engine 5 vs engine 4:", normwise_rel(U5, U4))
         elif a == "c3":
             U5 = timed(3, engine=5)
             U4 = timed(3, engine=4)
