@@ -113,7 +113,7 @@ typedef struct {
                               rows of a level on chip (du in registers, u^n and b in shared memory), the level solves are
                               engine 4's red-black SOR sweeps, strips of a set meet through neighbour exchange only
                               (even row count, strip heights that have an instantiation; constant-viscosity Burgers on
-                              periodic grids with 256 or 512 unknowns per row: pit_newton_ps.cuh; the general law — heat,
+                              periodic grids with 64, 256 or 512 unknowns per row: pit_newton_ps.cuh; the general law — heat,
                               Burgers with m2 > 0 — on Dirichlet or periodic grids with 256 unknowns per row:
                               pit_newton_ps0.cuh).  2/3/4/5: PIT_EINVAL if
                               they do not apply.  Level solves outside the Newton solve (pit_level_solve_device,
