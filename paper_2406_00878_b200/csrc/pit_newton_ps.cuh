@@ -62,32 +62,40 @@ struct PsEngine {
     static constexpr size_t OFF_E = OFF_A + (size_t)NB_NP * NTH;          // wedge [RG groups][2 kinds][HHM][NW] warp-edge E/W products
     static constexpr size_t OFF_G = OFF_E + (size_t)RG * 2 * HHM * NW;    // gx   [2 colours][2][T] N/S products across the row groups
     static constexpr size_t OFF_R = OFF_G + (size_t)4 * T;                // red  [RG NW][NB_NP]
-    static constexpr size_t SMEM = (OFF_R + (size_t)RG * NW * NB_NP) * sizeof(double);
+    static constexpr size_t OFF_S = OFF_R + (size_t)RG * NW * NB_NP;      // scalars shared by the two code paths (16 words)
+    static constexpr size_t SMEM = (OFF_S + 16) * sizeof(double);
 
     // HH = rows per thread (H = 2 HH rows per strip).  Row group g owns strip rows g HH .. g HH + HH - 1.  When HH is
     // odd the upper group starts on an odd row: its threads hold their two columns SWAPPED (local column jj = actual
     // column ^ f), so that the colour of local point (q, jj) is (q + jj) & 1 in both groups and every register
     // subscript stays compile-time; the E/W roles then mirror, which only flips the sign of ax and the shuffle
     // direction (per-thread constants).
-    template <int HH, bool ISO>
+    // The row group is a template parameter (the kernel branches once, per warp): the column swap, the strip side
+    // and every sign it implies are compile-time in each of the two code paths.
+    template <int HH, bool ISO, int GRP>
     __device__ __forceinline__ static void run(const PsParams& S, double* sm) {
         constexpr int H = RG * HH;
         const Prob P = S.P;
         const int Gs = S.Gs, c = blockIdx.x, p = c / Gs, s = c % Gs;
         const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-        const int g = RG == 2 ? tid / T : 0, t = tid % T, wl = w % NW;
+        constexpr int g = GRP;
+        const int t = tid % T, wl = w % NW;
         const int nyu = P.nyu, nt = P.nt, D = S.D, B = S.B;
         const long long ns = P.ns;
         const int na = (nyu - HE * Gs) / 2;                 // strips 0 .. na-1 have HE + 2 rows
         const int r0 = s * HE + 2 * min(s, na);             // first row of the strip (even)
         const int ss = s > 0 ? s - 1 : Gs - 1, sn = s + 1 < Gs ? s + 1 : 0;   // periodic neighbours (rows below / above)
-        const int f = (g * HH) & 1;                         // column swap of this thread (upper group, HH odd)
+        constexpr int f = (g * HH) & 1;                     // column swap of this thread (upper group, HH odd)
         const int c0 = 2 * t;
 
         // The iterate this solve will probably end in (the previous solve's count, a device word: no host round trip)
         // is written straight into u_out; slot 0 (U_0 / a caller's guess) never is.  A wrong guess costs the final copy.
         // (kept in shared memory: the sweeps have no register to spare)
-        __shared__ int s_alias;
+        long long* s_tr = reinterpret_cast<long long*>(sm + OFF_S);      // [PS_TR] cycle accounts
+        long long* s_tm = s_tr + PS_TR;                                    // [2]
+        int* s_dec = reinterpret_cast<int*>(s_tm + 2);                     // [2] the pass's decision
+        int& s_last = s_dec[2];
+        int& s_alias = s_dec[3];
         if (tid == 0) {
             const int hint = S.u_out ? __ldcg(S.hint) : 0;
             s_alias = (hint > 0 && hint % B != 0) ? hint % B : -1;
@@ -99,10 +107,6 @@ struct PsEngine {
         double* wedge = sm + OFF_E + (size_t)g * 2 * HHM * NW;   // this group's [2 kinds][HHM][NW]
         double* gx0 = sm + OFF_G;                            // per colour: [0][t] lower group's top row -> upper, [1][t] upper's bottom row -> lower
         double* red_s = sm + OFF_R;
-        __shared__ int s_dec[2];
-        __shared__ int s_last;
-        __shared__ long long s_tr[PS_TR];
-        __shared__ long long s_tm[2];
 
         // LL cells of a strip: [ring][side][t]; side 0 = its bottom row (published by the lower group), 1 = its top row
         unsigned long long* myx = S.llx + ((size_t)(p * Gs + s) * PS_RX * 2 * T) * 2;
@@ -613,10 +617,13 @@ __global__ void __launch_bounds__(RG * NXU / 2, 1) k_newton_ps(const PsParams S)
     const int s = blockIdx.x % S.Gs;
     const int na = (S.P.nyu - HE * S.Gs) / 2;
     const bool iso = S.ax == S.ay && S.bx == S.by;      // hx = hy: the y products of the sweeps are the x products
+    const bool up = RG == 2 && (int)threadIdx.x >= NXU / 2;      // the upper row group (warp-uniform)
     if (s < na) {
-        if (iso) E::template run<(HE + 2) / RG, true>(S, sm_ps); else E::template run<(HE + 2) / RG, false>(S, sm_ps);
+        if (iso) { if (up) E::template run<(HE + 2) / RG, true, RG - 1>(S, sm_ps); else E::template run<(HE + 2) / RG, true, 0>(S, sm_ps); }
+        else { if (up) E::template run<(HE + 2) / RG, false, RG - 1>(S, sm_ps); else E::template run<(HE + 2) / RG, false, 0>(S, sm_ps); }
     } else {
-        if (iso) E::template run<HE / RG, true>(S, sm_ps); else E::template run<HE / RG, false>(S, sm_ps);
+        if (iso) { if (up) E::template run<HE / RG, true, RG - 1>(S, sm_ps); else E::template run<HE / RG, true, 0>(S, sm_ps); }
+        else { if (up) E::template run<HE / RG, false, RG - 1>(S, sm_ps); else E::template run<HE / RG, false, 0>(S, sm_ps); }
     }
 }
 
