@@ -33,20 +33,22 @@ struct PsEngine0 {
     static constexpr size_t OFF_E = OFF_A + (size_t)NB_NP * NTH;          // wedge [RG groups][2 kinds][HHM][NWP] warp-edge values of du
     static constexpr size_t OFF_G = OFF_E + (size_t)RG * 2 * HHM * NWP;   // gx   [2 colours][2][T] du across the row groups
     static constexpr size_t OFF_R = OFF_G + (size_t)4 * T;                // red  [RG NW][NB_NP]
-    static constexpr size_t SMEM = (OFF_R + (size_t)RG * NW * NB_NP) * sizeof(double);
+    static constexpr size_t OFF_S = OFF_R + (size_t)RG * NW * NB_NP;      // scalars shared by the two code paths (16 words)
+    static constexpr size_t SMEM = (OFF_S + 16) * sizeof(double);
 
     // HH = rows per thread (H = 2 HH rows per strip).  Row group g owns strip rows g HH .. g HH + HH - 1.  When HH is
     // odd the upper group starts on an odd row: its threads hold their two columns SWAPPED (local column jj = actual
     // column ^ f), so that the colour of local point (q, jj) is (q + jj) & 1 in both groups and every register
     // subscript stays compile-time; the E/W roles then mirror, which only flips the sign of ax and the shuffle
     // direction (per-thread constants).
-    template <int HH>
+    template <int HH, int GRP>
     __device__ __forceinline__ static void run(const PsParams& S, double* sm) {
         constexpr int H = RG * HH;
         const Prob P = S.P;
         const int Gs = S.Gs, c = blockIdx.x, p = c / Gs, s = c % Gs;
         const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-        const int g = tid / T, t = tid % T, wl = w % NW;
+        constexpr int g = GRP;                              // the row group is compile-time (the kernel branches once, per warp)
+        const int t = tid % T, wl = w % NW;
         const int nyu = P.nyu, nt = P.nt, D = S.D, B = S.B;
         const long long ns = P.ns;
         const int na = (nyu - HE * Gs) / 2;                 // strips 0 .. na-1 have HE + 2 rows
@@ -54,13 +56,17 @@ struct PsEngine0 {
         // neighbouring strips (rows below / above); -1 = the grid's Dirichlet boundary
         const int ss = s > 0 ? s - 1 : (PER ? Gs - 1 : -1), sn = s + 1 < Gs ? s + 1 : (PER ? 0 : -1);
         const int nxp = P.nx + 1;                           // ring layout: bottom [nxp], top [nxp], left [ny-1], right [ny-1]
-        const int f = (g * HH) & 1;                         // column swap of this thread (upper group, HH odd)
+        constexpr int f = (g * HH) & 1;                     // column swap of this thread (upper group, HH odd)
         const int c0 = 2 * t;
 
         // The iterate this solve will probably end in (the previous solve's count, a device word: no host round trip)
         // is written straight into u_out; slot 0 (U_0 / a caller's guess) never is.  A wrong guess costs the final copy.
         // (kept in shared memory: the sweeps have no register to spare)
-        __shared__ int s_alias;
+        long long* s_tr = reinterpret_cast<long long*>(sm + OFF_S);      // [PS_TR] cycle accounts
+        long long* s_tm = s_tr + PS_TR;                                    // [2]
+        int* s_dec = reinterpret_cast<int*>(s_tm + 2);                     // [2] the pass's decision
+        int& s_last = s_dec[2];
+        int& s_alias = s_dec[3];
         if (tid == 0) {
             const int hint = S.u_out ? __ldcg(S.hint) : 0;
             s_alias = (hint > 0 && hint % B != 0) ? hint % B : -1;
@@ -73,10 +79,6 @@ struct PsEngine0 {
         double* wedge = sm + OFF_E + (size_t)g * 2 * HHM * NWP;  // this group's [2 kinds][HHM][NWP]
         double* gx0 = sm + OFF_G;                            // per colour: [0][t] lower group's top row -> upper, [1][t] upper's bottom row -> lower
         double* red_s = sm + OFF_R;
-        __shared__ int s_dec[2];
-        __shared__ int s_last;
-        __shared__ long long s_tr[PS_TR];
-        __shared__ long long s_tm[2];
 
         // LL cells of a strip: [ring][side][t]; side 0 = its bottom row (published by the lower group), 1 = its top row
         unsigned long long* myx = S.llx + ((size_t)(p * Gs + s) * PS_RX * 2 * T) * 2;
@@ -541,7 +543,9 @@ __global__ void __launch_bounds__(NXU, 1) k_newton_ps0(const PsParams S) {
     if ((int)blockIdx.x >= S.D * S.Gs) return;
     const int s = blockIdx.x % S.Gs;
     const int na = (S.P.nyu - HE * S.Gs) / 2;
-    if (s < na) E::template run<(HE + 2) / 2>(S, sm_ps0); else E::template run<HE / 2>(S, sm_ps0);
+    const bool up = (int)threadIdx.x >= NXU / 2;                 // the upper row group (warp-uniform)
+    if (s < na) { if (up) E::template run<(HE + 2) / 2, 1>(S, sm_ps0); else E::template run<(HE + 2) / 2, 0>(S, sm_ps0); }
+    else { if (up) E::template run<HE / 2, 1>(S, sm_ps0); else E::template run<HE / 2, 0>(S, sm_ps0); }
 }
 
 }  // namespace pit
