@@ -130,8 +130,7 @@ struct PsEngine {
         const double rsc = aC1 * (om1 / omega);                      // residual of a just-relaxed point: rsc (x_new - x_old)
         // kind A rows (other colour in local column 1): the product travels to thread t + 1 (f = 0) or t - 1 (f = 1);
         // kind B rows (other colour in local column 0): the opposite way.
-        int srcA = (lane + (f ? 1 : 31)) & 31, srcB = (lane + (f ? 31 : 1)) & 31;
-        asm volatile("" : "+r"(srcA), "+r"(srcB));
+        // (kind A values come from lane - 1 (f = 0) or lane + 1 (f = 1), kind B values from the other side)
         const int edgeA = f ? 31 : 0, edgeB = f ? 0 : 31;    // lanes whose source lies in the neighbouring warp
         const int wsA = f ? (wl + 1) % NW : (wl + NW - 1) % NW, wsB = f ? (wl + NW - 1) % NW : (wl + 1) % NW;
         double* wdA = wedge;                                 // [HHM][NW]
@@ -235,13 +234,13 @@ struct PsEngine {
                 // the travelling product goes to the neighbouring thread at once (shuffle); the lanes whose source lies in
                 // the neighbouring warp take theirs from shared memory behind the barrier instead
                 if (jn == 1) {               // kind A: in-thread term pa, travelling term pb
-                    const double in = __shfl_sync(0xffffffffu, pb, srcA);
+                    const double in = f ? __shfl_down_sync(0xffffffffu, pb, 1) : __shfl_up_sync(0xffffffffu, pb, 1);
                     tt[q] -= pa;
                     if (!isA) tt[q] -= in;
                     asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
                                  ::"r"(wdA_w + (unsigned)(q * NW * 8)), "d"(pb), "r"(wrA) : "memory");
                 } else {                     // kind B: in-thread term pb, travelling term pa
-                    const double in = __shfl_sync(0xffffffffu, pa, srcB);
+                    const double in = f ? __shfl_up_sync(0xffffffffu, pa, 1) : __shfl_down_sync(0xffffffffu, pa, 1);
                     tt[q] -= pb;
                     if (!isB) tt[q] -= in;
                     asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
