@@ -170,7 +170,10 @@ void pit_destroy(pit_handle* h);
  *   hist  [newton_max][4]  per iteration k: { rms R(U_k), max|R(U_k)|, rms dU_k, max|dU_k| }
  *                          (rms dU_k is the paper's "residual"); may be NULL
  *   n_iter                 iterations performed; may be NULL
- * Returns the solve status (PIT_OK / PIT_OK_FLOOR / PIT_ENOCONV / PIT_EBREAKDOWN) or an error. */
+ * Returns the solve status (PIT_OK / PIT_OK_FLOOR / PIT_ENOCONV / PIT_EBREAKDOWN) or an error.
+ * With engine 5, from the second call on a handle, the iterate the previous call ended in is streamed to u_out level by
+ * level while the kernel still runs (a copy stream follows the strips' level counters; pinned u_out overlaps fully);
+ * if this solve ends in another iteration the copy is redone after the kernel.  The result is the same either way. */
 int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* guess,
               double* u_out, double* hist, int32_t* n_iter);
 

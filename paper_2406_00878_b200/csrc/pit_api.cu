@@ -97,6 +97,11 @@ struct pit_handle {
     unsigned long long* ps_llx = nullptr;   // [D][Gs][PS_RX][2][nxu / 2] LL cells
     unsigned* ps_lvl = nullptr;             // [D][Gs] level counters
     int ps_rg = 2;                          // row groups per CTA (PIT_PS_DBG bit 2: the one-group experiment)
+    // pit_solve (host buffers) streams the probable final iterate to the host while engine 5 still runs
+    cudaStream_t ps_cs = nullptr;           // non-blocking copy stream
+    cudaEvent_t ps_ev_reset = nullptr;      // the level counters of this solve are cleared
+    unsigned* ps_h_lvl = nullptr;           // pinned host copy of the level counters
+    int ps_host_kf = 0;                     // Newton iterations of the previous pit_solve on this handle (0 = none)
     int* ps_hint = nullptr;                 // device word: Newton iterations of the previous engine-5 solve (0 = none)
     size_t ps_llx_bytes = 0;
     int last_engine = 0;          // engine of the last Newton solve
@@ -622,6 +627,9 @@ int pit_create_with_workspace(const pit_config* cfg, void* dev_ws, size_t bytes,
 void pit_destroy(pit_handle* h) {
     if (!h) return;
     cudaSetDevice(h->device);
+    if (h->ps_cs) cudaStreamDestroy(h->ps_cs);
+    if (h->ps_ev_reset) cudaEventDestroy(h->ps_ev_reset);
+    if (h->ps_h_lvl) cudaFreeHost(h->ps_h_lvl);
     free_all(h);
     delete h;
 }
@@ -778,6 +786,7 @@ static int launch_ps(pit_handle* h, const double* d_u0, const double* ring, doub
     CUDA_TRY(h, cudaEventRecord(h->ev[2], st));
     CUDA_TRY(h, cudaMemsetAsync(h->ps_llx, 0, h->ps_llx_bytes, st));
     CUDA_TRY(h, cudaMemsetAsync(h->ps_lvl, 0, sizeof(unsigned) * h->ps_D * h->ps_Gs, st));
+    if (h->ps_ev_reset) CUDA_TRY(h, cudaEventRecord(h->ps_ev_reset, st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_sync, 0, sizeof(unsigned) * 2 * MAXK, st));
     CUDA_TRY(h, cudaMemsetAsync(h->nb_linres, 0, sizeof(double) * 2 * MAXK, st));
     CUDA_TRY(h, cudaMemsetAsync(h->stats, 0, (8 + MAXK) * sizeof(long long), st));
@@ -1118,10 +1127,22 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
     CUDA_TRY(h, cudaMemset(h->hist, 0, sizeof(double) * 4 * h->cfg.newton_max));
     h->product_used = 0;
     const bool prod = want_product(h, has_bc ? h->d_bc : nullptr, 0);
+    bool stream_copy = false;
     if (prod) {
         rc = solve_product(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else if (h->ps) {
+        if (!h->ps_cs) {        // (first host-path solve on this handle) the streaming copy's stream, event and pinned counters
+            if (cudaStreamCreateWithFlags(&h->ps_cs, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&h->ps_ev_reset, cudaEventDisableTiming) != cudaSuccess ||
+                cudaHostAlloc((void**)&h->ps_h_lvl, sizeof(unsigned) * h->ps_D * h->ps_Gs, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                if (h->ps_cs) cudaStreamDestroy(h->ps_cs);
+                if (h->ps_ev_reset) cudaEventDestroy(h->ps_ev_reset);
+                h->ps_cs = nullptr; h->ps_ev_reset = nullptr; h->ps_h_lvl = nullptr;      // fall back to the copy after the solve
+            }
+        }
         rc = launch_ps(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0, ps_bcast);
+        stream_copy = rc == PIT_OK && h->ps_cs && h->ps_host_kf > 0;
     } else if (h->nb) {
         rc = launch_nb(h, h->d_u0, has_bc ? h->d_bc : nullptr, nullptr, h->hist, h->info, 0);
     } else {
@@ -1134,11 +1155,47 @@ int pit_solve(pit_handle* h, const double* u0, const double* bc, const double* g
         rc = launch_newton(h, S, 0);
     }
     if (rc != PIT_OK) return rc;
+    // Engine 5 writes iterate K level by level (set (K-1) % D, one level counter per strip, published behind a fence):
+    // with K guessed from the previous solve on this handle, the levels every strip has published are copied to the
+    // host WHILE the kernel runs (the copy stream reads the counters, then the rows, in stream order); if the solve
+    // ends in another iteration the copy is simply redone.  No kernel takes part in this.
+    int copied = 0;
+    const int Kg = h->ps_host_kf;
+    if (stream_copy) {
+        const int D5 = h->ps_D, Gs = h->ps_Gs, pset = (Kg - 1) % D5;
+        const long long pbase = (long long)((Kg - 1) / D5) * P.nt;
+        const double* Us = h->U + (long long)(Kg % h->B) * N;
+        const int chunk = std::max(1, (P.nt + 31) / 32);
+        CUDA_TRY(h, cudaStreamWaitEvent(h->ps_cs, h->ps_ev_reset, 0));
+        for (;;) {
+            const bool fin = cudaStreamQuery(0) == cudaSuccess;      // the kernel (and everything before it) has finished
+            CUDA_TRY(h, cudaMemcpyAsync(h->ps_h_lvl, h->ps_lvl, sizeof(unsigned) * D5 * Gs, cudaMemcpyDeviceToHost, h->ps_cs));
+            CUDA_TRY(h, cudaStreamSynchronize(h->ps_cs));
+            unsigned mn = 0xffffffffu;
+            for (int q = 0; q < Gs; ++q) mn = std::min(mn, h->ps_h_lvl[(size_t)pset * Gs + q]);
+            const long long done = std::max(0ll, std::min<long long>((long long)mn - pbase, P.nt));
+            while (copied < P.nt && (copied + chunk <= done || done == P.nt)) {
+                const int L = std::min(chunk, P.nt - copied);
+                CUDA_TRY(h, cudaMemcpyAsync(u_out + (long long)copied * P.ns, Us + (long long)copied * P.ns,
+                                            sizeof(double) * L * P.ns, cudaMemcpyDeviceToHost, h->ps_cs));
+                copied += L;
+            }
+            if (fin) break;
+        }
+        cudaGetLastError();      // (cudaStreamQuery's cudaErrorNotReady)
+    }
     int info[2];
     CUDA_TRY(h, cudaMemcpy(info, h->info, sizeof(info), cudaMemcpyDeviceToHost));
     const int kf = info[0];
     const double* Uf = prod ? h->U : h->U + (long long)(kf % h->B) * N;
-    CUDA_TRY(h, cudaMemcpy(u_out, Uf, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    if (stream_copy) {
+        CUDA_TRY(h, cudaStreamSynchronize(h->ps_cs));
+        if (kf != Kg) copied = 0;                                   // the guess was wrong: the rows copied so far are another iterate's
+    }
+    if (copied < P.nt)
+        CUDA_TRY(h, cudaMemcpy(u_out + (long long)copied * P.ns, Uf + (long long)copied * P.ns,
+                               sizeof(double) * (P.nt - copied) * P.ns, cudaMemcpyDeviceToHost));
+    if (h->ps && !prod) h->ps_host_kf = kf;
     if (hist) CUDA_TRY(h, cudaMemcpy(hist, h->hist, sizeof(double) * 4 * h->cfg.newton_max, cudaMemcpyDeviceToHost));
     if (n_iter) *n_iter = kf;
     return info[1];

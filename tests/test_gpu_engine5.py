@@ -209,3 +209,24 @@ def test_engine5_general_law_matches_oracle(name, make, depth):
     assert normwise_rel(U, seq.U) <= 1e-10, normwise_rel(U, seq.U)
     U4, h4, n4, s4, st4 = gpu_solve(p, engine=4)
     assert st4["engine"] == 4 and n4 == nit and normwise_rel(U, U4) <= 1e-12
+
+
+def test_engine5_host_path_streams_the_solution_out():
+    """pit_solve on a handle that has solved before copies the probable final iterate to the host level by level while
+    the kernel runs (the copy stream follows the strips' level counters): same bits as the first solve's copy after the
+    kernel; a changed iteration count (other data) falls back to the copy after the solve and is still right."""
+    p = W.config(5, nt=24)
+    s = pit.Solver(p, engine=5)
+    try:
+        U1, h1, n1, s1 = s.solve_host(p.u0, None)
+        U2, h2, n2, s2 = s.solve_host(p.u0, None)          # streamed
+        assert (n1, s1) == (n2, s2) and s1 in (0, 1)
+        assert np.array_equal(U1, U2) and np.array_equal(h1, h2)
+        U3, h3, n3, s3 = s.solve_host(0.25 * p.u0, None)    # guess of the final iterate may be wrong
+        U4, h4, n4, s4 = s.solve_host(0.25 * p.u0, None)
+        assert (n3, s3) == (n4, s4) and np.array_equal(U3, U4)
+    finally:
+        s.close()
+    q = W.custom("quarter", p.pde, p.bc, p.nx, p.ny, p.nt, p.dt, p.m0, p.m2, u0=0.25 * p.u0)
+    Uq, hq, nq, sq = pit.solve(q, engine=5)
+    assert nq == n3 and np.array_equal(Uq, U3)
