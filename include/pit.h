@@ -16,8 +16,9 @@
  * Newton's method for ALL levels at once (Eq. 5): every iteration forms the space-time residual and
  * the block-bidiagonal Jacobian of Eq. (6) (kernel a), applies its exact blockwise inverse Eq. (7)
  * (stage b: on-device level recurrence, or the literal Theorem 1 product form inside the paper's
- * Section 7 conditioning window), solves the per-level 5-point systems (stage c, batched
- * BiCGSTAB) and updates U, with convergence checked on the device (stage d).
+ * Section 7 conditioning window), solves the per-level 5-point systems (stage c: fixed-sweep
+ * red-black SOR in the default engines 4 and 5, Jacobi-scaled BiCGSTAB in engines 1-3) and updates
+ * U, with convergence checked on the device (stage d).
  *
  * Conventions
  *   Layout: fp64, row-major [n][j][i], i (x) fastest.  Level n = 1..nt is stored
