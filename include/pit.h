@@ -43,7 +43,9 @@
  *             PIT_X0=0           engines 2-3 start each level solve from 0 instead of the carry du^{n-1}
  *             PIT_MERGE=0        engine 3 without the merged first BiCGSTAB iteration
  *             PIT_GUESS_GRAPH=0  the coarse-grid guess's level march without a CUDA graph
- *             PIT_PS_DBG=1       engine 5 timing experiment: neighbour cells are not waited for (WRONG results)
+ *             PIT_PS_DBG         engine 5 experiments (with PIT_TRACE=1, the developer build of its kernels): bit 0 = neighbour cells
+ *                                are not waited for, bit 1 = no fence before the level counters (both WRONG results, timing only);
+ *                                bit 2 = one row group of 256 threads per CTA on 512-wide rows
  *           All NVTX ranges ("pit_solve_device", "pit_solve", ...) are emitted unconditionally (free without a tool).
  */
 #ifndef PIT_H

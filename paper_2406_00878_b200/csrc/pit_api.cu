@@ -310,8 +310,8 @@ static int create_impl(const pit_config* cfg, char* ws, size_t ws_size, bool mea
 
 // Engine 5 kernel for the handle's law, boundary condition and row length at base strip height he.
 static const void* ps_fn(const pit_handle* h, int he, size_t* smem, int* threads) {
-    return h->law == 1 ? ps_kernel_law1(h->P.nxu, he, h->ps_rg, smem, threads)
-                       : ps_kernel_law0(h->P.nxu, he, h->P.bc == PIT_PERIODIC ? 1 : 0, smem, threads);
+    return h->law == 1 ? ps_kernel_law1(h->P.nxu, he, h->ps_rg, h->dbg.trace, smem, threads)
+                       : ps_kernel_law0(h->P.nxu, he, h->P.bc == PIT_PERIODIC ? 1 : 0, h->dbg.trace, smem, threads);
 }
 
 // The c_f-coarsened problem of the initial guess: N_x / c_f, N_y / c_f intervals, N_t / c_f levels

@@ -16,7 +16,7 @@
 
 namespace pit {
 
-template <int NXU, int HE, bool PER>
+template <int NXU, int HE, bool PER, bool TRACE>
 struct PsEngine0 {
     static constexpr int RG = 2;
     static constexpr int T = NXU / 2;          // threads per row group (two columns each)
@@ -129,14 +129,14 @@ struct PsEngine0 {
         int lastx = -1;
         unsigned qx = 0;
         int levels = 0;
-        const bool trace = S.trace != nullptr && tid == 0;   // cycle accounts of thread 0, kept in shared memory
+        const bool trace = TRACE && S.trace != nullptr && tid == 0;   // cycle accounts of thread 0, kept in shared memory
         if (trace) {
             for (int i = 0; i < PS_TR; ++i) s_tr[i] = 0;
             s_tm[0] = s_tm[1] = clock64();
         }
         auto mark = [&](int i) { if (trace) { const long long now = clock64(); s_tr[i] += now - s_tm[1]; s_tm[1] = now; } };
         auto take = [&](const unsigned long long* q, LLc cl, unsigned fl) -> double {
-            if (S.dbg & 1) return __hiloint2double((int)(unsigned)cl.w1, (int)(unsigned)cl.w0);   // timing experiment: no wait
+            if (TRACE && (S.dbg & 1)) return __hiloint2double((int)(unsigned)cl.w1, (int)(unsigned)cl.w0);   // timing experiment: no wait
             if (trace) {
                 long long a = 0;
                 const double v = ll_take_t(q, cl, fl, a);
@@ -162,7 +162,7 @@ struct PsEngine0 {
                 if (sn >= 0) v2 = ps::ld_rlx(fprev + sn);
             }
             const bool ready = pf_lv && min(v0, min(v1, v2)) >= base + (unsigned)pf_lv;
-            if ((flag_lv || (ready && fprev)) && !(S.dbg & 2)) __threadfence();   // (dbg bit 1: timing experiment without the fence)
+            if ((flag_lv || (ready && fprev)) && !(TRACE && (S.dbg & 2))) __threadfence();   // (dbg bit 1: timing experiment without the fence)
             if (flag_lv) {
                 asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(fmine), "r"(base + (unsigned)flag_lv) : "memory");
                 flag_lv = 0;
@@ -536,10 +536,10 @@ struct PsEngine0 {
     }
 };
 
-template <int NXU, int HE, bool PER>
+template <int NXU, int HE, bool PER, bool TRACE>
 __global__ void __launch_bounds__(NXU, 1) k_newton_ps0(const PsParams S) {
     extern __shared__ __align__(128) double sm_ps0[];
-    using E = PsEngine0<NXU, HE, PER>;
+    using E = PsEngine0<NXU, HE, PER, TRACE>;
     if ((int)blockIdx.x >= S.D * S.Gs) return;
     const int s = blockIdx.x % S.Gs;
     const int na = (S.P.nyu - HE * S.Gs) / 2;

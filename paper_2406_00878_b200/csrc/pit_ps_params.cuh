@@ -37,9 +37,9 @@ struct PsParams {
 };
 
 // Implemented in pit_ps_law1.cu: the engine-5 kernel for (row length, base strip height), its dynamic shared memory
-// and threads; rg = row groups per CTA (2; 1 = the 256-thread experiment); nullptr if that shape has no instantiation.
-const void* ps_kernel_law1(int nxu, int he, int rg, size_t* smem, int* threads);
+// and threads; rg = row groups per CTA (2; 1 = the 256-thread experiment); trace = the developer build with cycle accounts (PIT_TRACE); nullptr if that shape has no instantiation.
+const void* ps_kernel_law1(int nxu, int he, int rg, bool trace, size_t* smem, int* threads);
 // Implemented in pit_ps_law0.cu (pit_newton_ps0.cuh): the general law, Dirichlet or periodic.
-const void* ps_kernel_law0(int nxu, int he, int periodic, size_t* smem, int* threads);
+const void* ps_kernel_law0(int nxu, int he, int periodic, bool trace, size_t* smem, int* threads);
 
 }  // namespace pit
