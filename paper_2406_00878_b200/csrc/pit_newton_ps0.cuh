@@ -182,24 +182,31 @@ struct PsEngine0 {
             if (ll) hc = ll_issue(g ? ncell(qn) : scell(qn));
             if (svc && tid == 0 && (flag_lv | pf_lv)) service(fbase);
             double* gx = gx0 + (size_t)cc * 2 * T;           // double-buffered: a fast warp's next half-sweep writes the other half
+            // (the loads of a row's right-hand side and coefficients run one row ahead of their use)
+            double nb_ = bsm(0, cc & 1), n0_ = cfm(0, 0, cc & 1), n1_ = cfm(1, 0, cc & 1), n2_ = cfm(2, 0, cc & 1), n3_ = cfm(3, 0, cc & 1);
             #pragma unroll
             for (int q = 0; q < HH; ++q) {
                 const int j = (q + cc) & 1, jn = 1 - j;
                 const double xq = x[q][jn];                   // this row's point of the other colour
-                double acc = fma(-cfm(0, q, j), xq, bsm(q, j));
+                const double cb = nb_, c0_ = n0_, c1_ = n1_, c2_ = n2_, c3_ = n3_;
+                if (q + 1 < HH) {
+                    const int j1 = (q + 1 + cc) & 1;
+                    nb_ = bsm(q + 1, j1); n0_ = cfm(0, q + 1, j1); n1_ = cfm(1, q + 1, j1); n2_ = cfm(2, q + 1, j1); n3_ = cfm(3, q + 1, j1);
+                }
+                double acc = fma(-c0_, xq, cb);
                 if (jn == 1) {               // kind A: the value travels as for the constant-viscosity law
                     const double in = __shfl_sync(0xffffffffu, xq, srcA);
-                    if (!isA) acc = fma(-cfm(1, q, j), in, acc);
+                    if (!isA) acc = fma(-c1_, in, acc);
                     asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
                                  ::"r"(wdA_w + (unsigned)(q * NWP * 8)), "d"(xq), "r"(wrA) : "memory");
                 } else {
                     const double in = __shfl_sync(0xffffffffu, xq, srcB);
-                    if (!isB) acc = fma(-cfm(1, q, j), in, acc);
+                    if (!isB) acc = fma(-c1_, in, acc);
                     asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
                                  ::"r"(wdB_w + (unsigned)(q * NWP * 8)), "d"(xq), "r"(wrB) : "memory");
                 }
-                if (q + 1 < HH) acc = fma(-cfm(2, q, j), x[q + 1 < HH ? q + 1 : q][j], acc);
-                if (q > 0) acc = fma(-cfm(3, q, j), x[q > 0 ? q - 1 : 0][j], acc);
+                if (q + 1 < HH) acc = fma(-c2_, x[q + 1 < HH ? q + 1 : q][j], acc);
+                if (q > 0) acc = fma(-c3_, x[q > 0 ? q - 1 : 0][j], acc);
                 tt[q] = acc;
             }
             // this group's boundary row towards the other group: its point of the other colour (raw du)
