@@ -216,14 +216,16 @@ struct PsEngine {
             }
             if (svc && tid == 0 && (flag_lv | pf_lv)) service(fbase);
             double* gx = gx0 + (size_t)cc * 2 * T;           // double-buffered: a fast warp's next half-sweep writes the other half
-            #pragma unroll
-            for (int q = 0; q < HH; ++q) tt[q] = bsm(q, (q + cc) & 1);
+            tt[0] = bsm(0, cc & 1);
+            double bnext = HH > 1 ? bsm(1, (1 + cc) & 1) : 0.0;      // (right-hand sides run one row ahead, like u)
             double unext = ub[(1 - (cc & 1)) ? uo1 : uo0];       // (the loads of u run one row ahead of their use: c5 23.9 -> 23.2 ms)
             #pragma unroll
             for (int q = 0; q < HH; ++q) {
                 const int jn = 1 - ((q + cc) & 1);               // the other colour's local column in this row
                 const double uq = unext, xq = x[q][jn];
                 if (q + 1 < HH) unext = ub[(size_t)(q + 1) * NXU + ((1 - ((q + 1 + cc) & 1)) ? uo1 : uo0)];
+                if (q + 1 < HH) tt[q + 1 < HH ? q + 1 : q] = bnext;
+                if (q + 2 < HH) bnext = bsm(q + 2, (q + 2 + cc) & 1);
                 // (a1 u - bx) x and (-a1 u - bx) x = -(a1 u - bx) x - 2 bx x; the same in y (on an isotropic grid the y
                 // products ARE the x products: the +a form is pa unless the columns are swapped)
                 const double pa = fma(a1, uq, -bx) * xq, pb = fma(-2.0 * bx, xq, -pa);
