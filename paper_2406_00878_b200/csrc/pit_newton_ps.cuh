@@ -243,14 +243,12 @@ struct PsEngine {
                     const double in = f ? __shfl_down_sync(0xffffffffu, pb, 1) : __shfl_up_sync(0xffffffffu, pb, 1);
                     tt[q] -= pa;
                     if (!isA) tt[q] -= in;
-                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
-                                 ::"r"(wdA_w + (unsigned)(q * NW * 8)), "d"(pb), "r"(wrA) : "memory");
+                    if (wrA) wdA[q * NW + wl] = pb;
                 } else {                     // kind B: in-thread term pb, travelling term pa
                     const double in = f ? __shfl_up_sync(0xffffffffu, pa, 1) : __shfl_down_sync(0xffffffffu, pa, 1);
                     tt[q] -= pb;
                     if (!isB) tt[q] -= in;
-                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
-                                 ::"r"(wdB_w + (unsigned)(q * NW * 8)), "d"(pa), "r"(wrB) : "memory");
+                    if (wrB) wdB[q * NW + wl] = pa;
                 }
                 if (q > 0) tt[q > 0 ? q - 1 : 0] -= pn;
                 else if (RG == 2 && g == 1) gx[T + t] = pn;  // to the lower group's top row
