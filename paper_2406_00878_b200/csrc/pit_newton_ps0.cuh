@@ -197,13 +197,11 @@ struct PsEngine0 {
                 if (jn == 1) {               // kind A: the value travels as for the constant-viscosity law
                     const double in = __shfl_sync(0xffffffffu, xq, srcA);
                     if (!isA) acc = fma(-c1_, in, acc);
-                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
-                                 ::"r"(wdA_w + (unsigned)(q * NWP * 8)), "d"(xq), "r"(wrA) : "memory");
+                    if (wrA) wdA[q * NWP + wl] = xq;
                 } else {
                     const double in = __shfl_sync(0xffffffffu, xq, srcB);
                     if (!isB) acc = fma(-c1_, in, acc);
-                    asm volatile("{ .reg .pred p; setp.ne.s32 p, %2, 0; @p st.shared.f64 [%0], %1; }"
-                                 ::"r"(wdB_w + (unsigned)(q * NWP * 8)), "d"(xq), "r"(wrB) : "memory");
+                    if (wrB) wdB[q * NWP + wl] = xq;
                 }
                 if (q + 1 < HH) acc = fma(-c2_, x[q + 1 < HH ? q + 1 : q][j], acc);
                 if (q > 0) acc = fma(-c3_, x[q > 0 ? q - 1 : 0][j], acc);
