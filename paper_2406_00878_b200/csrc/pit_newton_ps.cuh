@@ -138,6 +138,7 @@ struct PsEngine {
         double* wdA = wedge;                                 // [HHM][NW]
         double* wdB = wedge + (size_t)HHM * NW;
         int isA = lane == edgeA, isB = lane == edgeB;         // this lane's kind A / B source lies in the neighbouring warp
+        const double mA = isA ? 0.0 : 1.0, mB = isB ? 0.0 : 1.0;
         int wrA = lane == 31 - edgeA, wrB = lane == 31 - edgeB;   // this lane's kind A / B product is a neighbouring warp's source
         unsigned wdA_w = (unsigned)__cvta_generic_to_shared(wdA + wl), wdB_w = (unsigned)__cvta_generic_to_shared(wdB + wl);
         // (opaque to the compiler, which otherwise rebuilds these from the thread index in every row of the sweeps)
@@ -242,12 +243,12 @@ struct PsEngine {
                 if (jn == 1) {               // kind A: in-thread term pa, travelling term pb
                     const double in = f ? __shfl_down_sync(0xffffffffu, pb, 1) : __shfl_up_sync(0xffffffffu, pb, 1);
                     tt[q] -= pa;
-                    if (!isA) tt[q] -= in;
+                    tt[q] = fma(-mA, in, tt[q]);             // (mA = 0 on the lane whose source lies in the neighbouring warp)
                     if (wrA) wdA[q * NW + wl] = pb;
                 } else {                     // kind B: in-thread term pb, travelling term pa
                     const double in = f ? __shfl_up_sync(0xffffffffu, pa, 1) : __shfl_down_sync(0xffffffffu, pa, 1);
                     tt[q] -= pb;
-                    if (!isB) tt[q] -= in;
+                    tt[q] = fma(-mB, in, tt[q]);
                     if (wrB) wdB[q * NW + wl] = pa;
                 }
                 if (q > 0) tt[q > 0 ? q - 1 : 0] -= pn;
