@@ -257,15 +257,12 @@ struct PsEngine {
                 else if (RG == 2 && g == 0) gx[t] = psv;     // to the upper group's bottom row
             }
             cbar();
-            if (isA) {
-                #pragma unroll
-                for (int q = 0; q < HH; ++q)
-                    if ((q + cc) & 1) {} else tt[q] -= wdA[q * NW + wsA];      // kind A rows: other colour in local column 1
-            }
-            if (isB) {
-                #pragma unroll
-                for (int q = 0; q < HH; ++q)
-                    if ((q + cc) & 1) tt[q] -= wdB[q * NW + wsB];              // kind B rows
+            // the edge lanes' travelling products, from the neighbouring warp (every lane loads the broadcast value; the
+            // complementary 0/1 factor keeps it out of the other lanes: no divergent branch)
+            #pragma unroll
+            for (int q = 0; q < HH; ++q) {
+                if ((q + cc) & 1) tt[q] = fma(mB - 1.0, wdB[q * NW + wsB], tt[q]);      // kind B rows
+                else tt[q] = fma(mA - 1.0, wdA[q * NW + wsA], tt[q]);                   // kind A rows: other colour in local column 1
             }
             // the row below local row 0 and the row above local row HH-1: the other row group or the neighbouring strip
             if (RG == 2) {
