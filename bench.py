@@ -17,6 +17,7 @@ workload; rank 0 only.
 import argparse
 import json
 import os
+import datetime
 import statistics
 import subprocess
 import sys
@@ -44,46 +45,77 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line).  The sampler is started before the
+    warm-up (nvidia-smi takes longer to start than a short timed region lasts); only rows stamped inside the window
+    [mark(), stop()] count.  The caller keeps the same workload running, untimed, after the timed steps until the window
+    is long enough to hold a few samples."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    MIN_WINDOW_S = 1.5
 
     def __init__(self, index):
         self.index = index
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
+        self.t_mark = self.t_stop = None
 
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
         return self
 
-    def __exit__(self, *a):
+    def mark(self):
+        self.t_mark = datetime.datetime.now()
+
+    def window_s(self):
+        return (datetime.datetime.now() - self.t_mark).total_seconds() if self.t_mark else 0.0
+
+    def stop(self):
+        if self.t_stop is None:
+            self.t_stop = datetime.datetime.now()
         if self.p:
             self.p.terminate()
             try:
                 self.p.wait(timeout=5)
             except Exception:
                 self.p.kill()
+            self.p = None
+
+    def __exit__(self, *a):
+        self.stop()
 
     def summary(self):
         self.f.flush()
         try:
-            rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+            rows = [[c.strip() for c in l.split(",")] for l in open(self.f.name).read().strip().splitlines()
+                    if l.strip()]
         except Exception:
             rows = []
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        rows = [r for r in rows if len(r) >= 10]
+
+        def inside(r):
+            try:
+                t = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f")
+            except Exception:
+                return True
+            return (self.t_mark is None or t >= self.t_mark) and (self.t_stop is None or t <= self.t_stop)
+
+        win = [r for r in rows if inside(r)]
+        isnum = lambda x: x.replace(".", "").isdigit()
+        sm = [float(r[2]) for r in win if isnum(r[2])]
+        mx = [float(r[3]) for r in win if isnum(r[3])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        reasons = sorted({names[i] for r in win for i in range(4) if r[6 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(win), "samples_total": len(rows),
+                "window": "timed steps + untimed repeats of the same solve, back to back, until the window holds "
+                          f">= {self.MIN_WINDOW_S} s of load"}
 
 
 def cpu_info():
@@ -315,14 +347,16 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
+    clk = Clocks(local).__enter__()    # started before the warm-up: nvidia-smi needs longer to start than c5's timed region
     for _ in range(args.warmup):
         s.solve_device(d_u0, d_ring, None, d_out, d_hist, d_info, stream=stream)
     barrier()
     nit, status = (int(v) for v in d_info.cpu())
     newton_ms, launches = [], 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    try:
         barrier()
+        clk.mark()
         e0.record(stream)
         for _ in range(args.steps):
             s.solve_device(d_u0, d_ring, None, d_out, d_hist, d_info, stream=stream)
@@ -331,6 +365,12 @@ def main():
             launches += st["launches"]
         e1.record(stream)
         barrier()
+        # the clock samples need a longer window under load than K short steps: the same solve repeated, untimed
+        while clk.window_s() < clk.MIN_WINDOW_S:
+            s.solve_device(d_u0, d_ring, None, d_out, d_hist, d_info, stream=stream)
+            torch.cuda.synchronize(dev)
+    finally:
+        clk.stop()
     elapsed_ms = e0.elapsed_time(e1)
     nit, status = (int(v) for v in d_info.cpu())
     ei = s.engine_info()
